@@ -1,0 +1,133 @@
+/*
+ * sampleattn.h — C ABI of the B200-native SampleAttention hot path.
+ *
+ * The reference (`blocksift`, pure Python/numpy) exposes the hot path as the
+ * per-head body of run_pipeline (pkg/src/blocksift/pipeline.py:169-176):
+ *
+ *   sample_scores + block_reduce  -> sa_stage1          (stage 1, sampler.py:135-191)
+ *   find_k + arg_topk             -> sa_select          (stage 2a, filtering.py:30-62, 245-255)
+ *   merge_index                   -> sa_merge           (stage 2b, filtering.py:198-230)
+ *   sparse_attention              -> sa_sparse_forward  (stage 3, executor.py:104-158)
+ *
+ * plus helpers the Python host layer needs (workspace sizing, the finite
+ * check of core.py:30-37 / as_matrix, the LPT work order, a dense causal mask
+ * for the dense comparison row).
+ *
+ * Conventions (all entry points):
+ *   - plain device pointers and sizes; no framework types; the caller owns
+ *     every buffer (inputs, outputs, workspace); the library never allocates
+ *     device memory and never synchronises the stream;
+ *   - q is [Hq][S][d], k and v are [Hkv][S][d], out is [Hq][S][d], all
+ *     contiguous; q head h reads kv head (q_head0 + h)/group - q_head0/group
+ *     (GQA/MQA: group = Hq_total / Hkv_total; q_head0 = global index of the
+ *     first local q head, for head-sharded multi-GPU runs);
+ *   - dtype: SA_BF16 (tensor-core path, d == 128 and blk == 128 only) or
+ *     SA_FP32 (exact SIMT path, 1 <= d <= 128, 1 <= blk <= 128);
+ *   - the return value is SA_OK or a negative status; sa_last_error() gives
+ *     a thread-local message.  SA_ERR_INVALID / SA_ERR_UNSUPPORTED map to the
+ *     reference's InputError (exceptions.py:4), SA_ERR_INTERNAL to
+ *     InternalInvariantError (exceptions.py:16).
+ *
+ * Stage-1/2 block-score layout: col and slash are fp64 [Hq][cn][nb]
+ * (nb = ceil(S/blk)), the ChunkScores.col_scores / slash_scores of
+ * sampler.py:152-165.  Selections: k_out [Hq][cn][2] (k_c, k_s) and
+ * idx_out [Hq][cn][2][nb] (ascending i_c, i_s — filtering.py:65-76).
+ * Block mask (padded CSR): kv_cnt [Hq][nb] and kv_idx [Hq][nb*(nb+1)/2],
+ * query block qb's ascending key blocks at kv_idx + h*nb*(nb+1)/2 + qb*(qb+1)/2
+ * (BlockMask.active_for, filtering.py:128-130).
+ */
+#ifndef SAMPLEATTN_H_
+#define SAMPLEATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SA_OK 0
+#define SA_ERR_INVALID (-1)     /* bad argument (InputError) */
+#define SA_ERR_UNSUPPORTED (-2) /* shape/dtype the kernels do not specialise (InputError) */
+#define SA_ERR_INTERNAL (-3)    /* self-check failed (InternalInvariantError) */
+#define SA_ERR_CUDA (-4)        /* CUDA launch / driver failure */
+
+#define SA_BF16 0
+#define SA_FP32 1
+
+/* stage-1 precision modes */
+#define SA_STAGE1_TENSOR 0 /* tcgen05 bf16 x bf16 -> fp32 (bf16 only) */
+#define SA_STAGE1_EXACT 1  /* fp64 SIMT; bit-for-bit selection guard */
+
+int sa_version(void);
+const char* sa_last_error(void);
+/* Number of kernels this library has launched in the calling process
+ * (monotonic; the bench reports deltas as gpu_launches). */
+long long sa_launch_count(void);
+
+/* Bytes of scratch the stage-1/2/3 calls need for this geometry. */
+size_t sa_workspace_bytes(int S, int Hq, int Hkv, int d, int blk, int chunk_n, int dtype);
+
+/* Replaces the finite check of core.py:30-37 (as_matrix): *flag_dev is set
+ * to 1 (never cleared) when any of the n elements is NaN or Inf. */
+int sa_check_finite(const void* x, int dtype, int64_t n, int* flag_dev, void* stream);
+
+/* Stage 1 — replaces sample_scores + block_reduce (sampler.py:135-191) for
+ * every q head and every chunk of the plan (plan_chunks, sampler.py:88-118:
+ * window i samples rows [max(0, (i+1)*itv - blk), (i+1)*itv)).
+ * Writes col/slash [Hq][cn][nb] fp64.  mode: SA_STAGE1_TENSOR or
+ * SA_STAGE1_EXACT.  When only_flags != NULL, only (h, c) pairs with
+ * only_flags[h*cn + c] != 0 are (re)computed (the exact re-score of pairs
+ * sa_select flagged as too close to call). */
+int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, int d, int blk,
+              int group, int q_head0, int chunk_n, int itv, double* col, double* slash,
+              int mode, const int* only_flags, void* workspace, size_t workspace_bytes,
+              void* stream);
+
+/* Stage 2a — replaces find_k + arg_topk per (head, chunk, direction)
+ * (filtering.py:30-62, applied as in select_and_merge :245-255).
+ * margin_eps > 0 enables the selection guard: flags[h*cn + c] is set to 1
+ * when the alpha cut or the boundary tie gap lies within margin_eps * total
+ * of a decision, i.e. when scores carrying that relative error could change
+ * the reference's answer.  With only_flags != NULL only flagged pairs are
+ * recomputed.  k_in != NULL ([Hq][cn][2]) skips find_k and takes the given k
+ * (the reference's arg_topk(scores, k), filtering.py:51-62). */
+int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int nb,
+              double alpha_c, double alpha_s, double margin_eps, int* flags,
+              const int* only_flags, const int* k_in, int* k_out, int* idx_out, void* stream);
+
+/* Stage 2b — replaces merge_index (filtering.py:198-230): extends every
+ * chunk's picks over its query region, unions straddling blocks, forces the
+ * diagonal.  Writes the padded CSR and, when non-NULL, per-head totals:
+ * active_blocks[Hq] (BlockMask.active_count, filtering.py:118-119) and
+ * active_entries[Hq] (active_causal_entries, filtering.py:148-164).
+ * sink_blocks / local_blocks: optional forced key blocks [0, sink_blocks) and
+ * [qb - local_blocks + 1, qb] for every query block; the defaults (0, 1)
+ * reproduce the reference exactly (only the diagonal is forced). */
+int sa_merge(const int* k_sel, const int* idx_sel, int Hq, int chunk_n, int nb, int S, int blk,
+             int itv, int sink_blocks, int local_blocks, int* kv_cnt, int* kv_idx,
+             long long* active_blocks, long long* active_entries, void* stream);
+
+/* Full causal block mask (every kb <= qb): the dense-attention comparison row. */
+int sa_full_mask(int Hq, int nb, int* kv_cnt, int* kv_idx, void* stream);
+
+/* Longest-first work order over (head, query block) items from kv_cnt:
+ * order[i] = h*nb + qb, sorted by descending block count. */
+int sa_schedule(const int* kv_cnt, int Hq, int nb, int* order, void* workspace,
+                size_t workspace_bytes, void* stream);
+
+/* Stage 3 — replaces sparse_attention (executor.py:104-158): per (head,
+ * query block) the online-softmax recurrence over the mask's ascending key
+ * blocks, entry-level causality inside the diagonal block.  out is
+ * [Hq][S][d] in the input dtype; lse [Hq][S] fp32 (natural log) and
+ * touched[Hq] (blocks processed, FlopReport.active_blocks) are optional.
+ * order may be NULL (natural order). */
+int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, int S, int Hq,
+                      int Hkv, int d, int blk, int group, int q_head0, const int* kv_cnt,
+                      const int* kv_idx, const int* order, void* out, float* lse,
+                      long long* touched, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAMPLEATTN_H_ */

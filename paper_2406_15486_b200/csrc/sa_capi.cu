@@ -1,0 +1,221 @@
+// extern "C" boundary of libsampleattn (declared in include/sampleattn.h).
+//
+// Argument validation mirrors the reference's InputError checks
+// (sampler.py:52-56 SparseConfig, filtering.py:37-43 find_k, core.py:30-37
+// as_matrix); kernel dispatch picks the tcgen05 path for bf16 (d == blk == 128)
+// and the exact SIMT path for fp32.  No allocation, no stream synchronisation.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <atomic>
+#include <mutex>
+#include <string>
+
+#include "sa_internal.h"
+
+namespace sa {
+
+int launch_select(const double* col, const double* slash, int Hq, int cn, int nb, double ac,
+                  double as, double eps, int* flags, const int* only, const int* k_in, int* k_out,
+                  int* idx_out, cudaStream_t st);
+int launch_merge(const int* k_sel, const int* idx_sel, int Hq, int cn, int nb, int S, int blk,
+                 int itv, int sink_blocks, int local_blocks, int* kv_cnt, int* kv_idx,
+                 long long* ab, long long* ae, cudaStream_t st);
+int launch_full(int Hq, int nb, int* kv_cnt, int* kv_idx, cudaStream_t st);
+int launch_sched(const int* kv_cnt, int n_items, int nb, int* order, cudaStream_t st);
+int launch_check_finite(const void* x, int dtype, long long n, int* flag, cudaStream_t st);
+
+namespace {
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return SA_OK;
+}
+
+bool make_tmap_bf16_hsd(CUtensorMap* map, const void* base, int H, int S, int d) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)S, (cuuint64_t)H};
+  const cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)S * d * 2};
+  const cuuint32_t box[3] = {64, 128, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int dtype) {
+  (void)Hkv;
+  (void)d;
+  Workspace L{};
+  const int nb = ceil_div(S, blk);
+  const size_t rows = (size_t)Hq * cn * blk;
+  size_t off = 0;
+  L.tc_part = off;
+  if (dtype == SA_BF16) off = align_up(off + (size_t)3 * Hq * cn * 128 * nb * sizeof(float));
+  L.rowstat = off;
+  off = align_up(off + rows * 2 * sizeof(double));
+  L.nsx = ceil_div(nb, kExactKbPerCta);
+  L.x_part = off;
+  off = align_up(off + rows * L.nsx * 2 * sizeof(double));
+  L.part3 = off;
+  off = align_up(off + (size_t)Hq * cn * nb * 4 * sizeof(double));
+  L.sched = off;
+  off = align_up(off + (size_t)(nb + 2) * sizeof(int));
+  L.total = off;
+  return L;
+}
+
+}  // namespace sa
+
+using namespace sa;
+
+namespace {
+int check_geom(int S, int Hq, int Hkv, int d, int blk, int group, int q_head0, int dtype) {
+  if (S < 1 || Hq < 1 || Hkv < 1 || d < 1 || blk < 1)
+    return fail(SA_ERR_INVALID, "S, heads, d and blk must all be >= 1");
+  if (group < 1 || q_head0 < 0) return fail(SA_ERR_INVALID, "group must be >= 1, q_head0 >= 0");
+  if (kv_head_of(Hq - 1, group, q_head0) >= Hkv)
+    return fail(SA_ERR_INVALID, "q heads map past the supplied kv heads");
+  if (dtype == SA_BF16) {
+    if (d != kHeadDim || blk != kBlk)
+      return fail(SA_ERR_UNSUPPORTED, "bf16 tensor-core path needs d == 128 and blk == 128");
+  } else if (dtype == SA_FP32) {
+    if (d > kMaxSimtD || blk > kMaxSimtBlk)
+      return fail(SA_ERR_UNSUPPORTED, "fp32 path supports d <= 128 and blk <= 128");
+  } else {
+    return fail(SA_ERR_INVALID, "dtype must be SA_BF16 or SA_FP32");
+  }
+  return SA_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int sa_version(void) { return 100; }
+
+const char* sa_last_error(void) { return g_err.c_str(); }
+
+long long sa_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+size_t sa_workspace_bytes(int S, int Hq, int Hkv, int d, int blk, int chunk_n, int dtype) {
+  if (S < 1 || Hq < 1 || blk < 1 || chunk_n < 1) return 0;
+  return workspace_layout(S, Hq, Hkv, d, blk, chunk_n, dtype).total;
+}
+
+int sa_check_finite(const void* x, int dtype, int64_t n, int* flag_dev, void* stream) {
+  if (!x || !flag_dev) return fail(SA_ERR_INVALID, "sa_check_finite: null pointer");
+  return launch_check_finite(x, dtype, n, flag_dev, static_cast<cudaStream_t>(stream));
+}
+
+int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, int d, int blk,
+              int group, int q_head0, int chunk_n, int itv, double* col, double* slash, int mode,
+              const int* only_flags, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int e = check_geom(S, Hq, Hkv, d, blk, group, q_head0, dtype)) return e;
+  if (!q || !k || !col || !slash || !workspace) return fail(SA_ERR_INVALID, "sa_stage1: null pointer");
+  if (chunk_n < 1 || itv < 1) return fail(SA_ERR_INVALID, "sa_stage1: chunk_n and itv must be >= 1");
+  if (S >= blk && ((long long)chunk_n * itv > S || itv < blk))
+    return fail(SA_ERR_INVALID, "sa_stage1: (chunk_n, itv) is not a plan_chunks layout");
+  if (S < blk && (chunk_n != 1 || itv != S))
+    return fail(SA_ERR_INVALID, "sa_stage1: S < blk needs chunk_n == 1, itv == S");
+  const Workspace L = workspace_layout(S, Hq, Hkv, d, blk, chunk_n, dtype);
+  if (workspace_bytes < L.total) return fail(SA_ERR_INVALID, "sa_stage1: workspace too small");
+  Stage1Geom g{S, Hq, Hkv, d, blk, group, q_head0, chunk_n, itv, ceil_div(S, blk)};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  if (mode == SA_STAGE1_TENSOR) {
+    if (dtype != SA_BF16) return fail(SA_ERR_UNSUPPORTED, "tensor-core stage 1 needs bf16 inputs");
+    return launch_stage1_tc(g, q, k, only_flags, ws, L, col, slash, st);
+  }
+  if (mode == SA_STAGE1_EXACT)
+    return launch_stage1_exact(g, q, k, dtype, only_flags, ws, L, col, slash, st);
+  return fail(SA_ERR_INVALID, "sa_stage1: unknown mode");
+}
+
+int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int nb, double alpha_c,
+              double alpha_s, double margin_eps, int* flags, const int* only_flags, const int* k_in,
+              int* k_out, int* idx_out, void* stream) {
+  if (!(alpha_c >= 0.0 && alpha_c <= 1.0))
+    return fail(SA_ERR_INVALID, "alpha_c must be in [0, 1]");
+  if (!(alpha_s >= 0.0 && alpha_s <= 1.0))
+    return fail(SA_ERR_INVALID, "alpha_s must be in [0, 1]");
+  if (Hq < 1 || chunk_n < 1 || nb < 1) return fail(SA_ERR_INVALID, "sa_select: empty geometry");
+  if (!col || !slash || !k_out || !idx_out) return fail(SA_ERR_INVALID, "sa_select: null pointer");
+  if (margin_eps > 0.0 && !flags) return fail(SA_ERR_INVALID, "sa_select: guard needs flags");
+  return launch_select(col, slash, Hq, chunk_n, nb, alpha_c, alpha_s, margin_eps, flags, only_flags,
+                       k_in, k_out, idx_out, static_cast<cudaStream_t>(stream));
+}
+
+int sa_merge(const int* k_sel, const int* idx_sel, int Hq, int chunk_n, int nb, int S, int blk,
+             int itv, int sink_blocks, int local_blocks, int* kv_cnt, int* kv_idx,
+             long long* active_blocks, long long* active_entries, void* stream) {
+  if (Hq < 1 || chunk_n < 1 || S < 1 || blk < 1 || itv < 1 || nb != ceil_div(S, blk))
+    return fail(SA_ERR_INVALID, "sa_merge: inconsistent geometry");
+  if (sink_blocks < 0 || local_blocks < 1)
+    return fail(SA_ERR_INVALID, "sa_merge: sink_blocks must be >= 0 and local_blocks >= 1");
+  if (!k_sel || !idx_sel || !kv_cnt || !kv_idx) return fail(SA_ERR_INVALID, "sa_merge: null pointer");
+  return launch_merge(k_sel, idx_sel, Hq, chunk_n, nb, S, blk, itv, sink_blocks, local_blocks, kv_cnt,
+                      kv_idx, active_blocks, active_entries, static_cast<cudaStream_t>(stream));
+}
+
+int sa_full_mask(int Hq, int nb, int* kv_cnt, int* kv_idx, void* stream) {
+  if (Hq < 1 || nb < 1 || !kv_cnt || !kv_idx) return fail(SA_ERR_INVALID, "sa_full_mask: bad args");
+  return launch_full(Hq, nb, kv_cnt, kv_idx, static_cast<cudaStream_t>(stream));
+}
+
+int sa_schedule(const int* kv_cnt, int Hq, int nb, int* order, void* workspace,
+                size_t workspace_bytes, void* stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  if (Hq < 1 || nb < 1 || !kv_cnt || !order) return fail(SA_ERR_INVALID, "sa_schedule: bad args");
+  return launch_sched(kv_cnt, Hq * nb, nb, order, static_cast<cudaStream_t>(stream));
+}
+
+int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, int S, int Hq, int Hkv,
+                      int d, int blk, int group, int q_head0, const int* kv_cnt, const int* kv_idx,
+                      const int* order, void* out, float* lse, long long* touched, void* stream) {
+  if (int e = check_geom(S, Hq, Hkv, d, blk, group, q_head0, dtype)) return e;
+  if (!q || !k || !v || !kv_cnt || !kv_idx || !out)
+    return fail(SA_ERR_INVALID, "sa_sparse_forward: null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == SA_BF16)
+    return launch_sparse_tc(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse,
+                            touched, st);
+  return launch_sparse_simt(static_cast<const float*>(q), static_cast<const float*>(k),
+                            static_cast<const float*>(v), S, Hq, Hkv, d, blk, group, q_head0, kv_cnt,
+                            kv_idx, order, static_cast<float*>(out), lse, touched, st);
+}
+
+}  // extern "C"

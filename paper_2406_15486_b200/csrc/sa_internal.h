@@ -1,0 +1,70 @@
+// Internal declarations shared by the SampleAttention CUDA translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "sampleattn.h"
+
+namespace sa {
+
+// Thread-local error message behind sa_last_error().
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int check_launch(const char* what);
+
+constexpr int kBlk = 128;       // tensor-core tile (query rows == key rows == blk)
+constexpr int kHeadDim = 128;   // tensor-core head dimension
+constexpr int kMaxSimtD = 128;  // SIMT paths
+constexpr int kMaxSimtBlk = 128;
+constexpr int kExactKbPerCta = 16;  // exact stage-1: key blocks per CTA in the stats pass
+
+__host__ __device__ inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+__host__ __device__ inline long long tri(long long n) { return n * (n + 1) / 2; }
+
+// Geometry of one stage-1 call.
+struct Stage1Geom {
+  int S, Hq, Hkv, d, blk, group, q_head0, cn, itv, nb;
+};
+
+// Workspace carve-up (byte offsets), identical for every call of a geometry.
+struct Workspace {
+  size_t tc_part;   // float  [3][Hq*cn*blk*nb]   (A, B, m) per (row, key block)
+  size_t rowstat;   // double [Hq*cn*blk][2]      (log2 max, sum) per sampled row
+  size_t x_part;    // double [Hq*cn*blk*nsx][2]  exact stats per (row, key split)
+  size_t part3;     // double [Hq*cn*nb][4]       (col, slash X-1, X, X+1) per key block
+  size_t sched;     // int    [nb + 2]
+  size_t total;
+  int nsx;
+};
+Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int dtype);
+
+// Launchers (return SA_OK or an error code; all stream-ordered).
+int launch_stage1_exact(const Stage1Geom& g, const void* q, const void* k, int dtype,
+                        const int* only_flags, char* ws, const Workspace& L, double* col,
+                        double* slash, cudaStream_t st);
+int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const int* only_flags,
+                     char* ws, const Workspace& L, double* col, double* slash, cudaStream_t st);
+int launch_stage1_finalize(const Stage1Geom& g, const int* only_flags, const double* part3,
+                           double* col, double* slash, cudaStream_t st);
+
+int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq, int Hkv,
+                     int group, int q_head0, const int* kv_cnt, const int* kv_idx,
+                     const int* order, void* out, float* lse, long long* touched,
+                     cudaStream_t st);
+int launch_sparse_simt(const float* q, const float* k, const float* v, int S, int Hq, int Hkv,
+                       int d, int blk, int group, int q_head0, const int* kv_cnt,
+                       const int* kv_idx, const int* order, float* out, float* lse,
+                       long long* touched, cudaStream_t st);
+
+// TMA descriptor for a contiguous [H][S][d] bf16 tensor, box {64, 128, 1}, 128B swizzle.
+bool make_tmap_bf16_hsd(CUtensorMap* map, const void* base, int H, int S, int d);
+
+__host__ __device__ inline int kv_head_of(int h, int group, int q_head0) {
+  return (q_head0 + h) / group - q_head0 / group;
+}
+
+}  // namespace sa

@@ -1,0 +1,270 @@
+// Stage 3, tensor-core mode: block-sparse causal attention prefill on sm_100a
+// (replaces sparse_attention, ref pkg/src/blocksift/executor.py:104-158).
+//
+// One CTA = one (q head, 128-row query block) work item, taken in the
+// longest-first order produced by sa_schedule.  The item's ascending key-block
+// list (the merged column + slash + diagonal mask of stage 2) drives:
+//   warp 0   TMA producer: Q once, then K and V tiles of each listed block
+//   warp 1   tcgen05 issuer: S = Q K^T into TMEM cols [0,128); after the
+//            softmax has overwritten S with bf16 P (cols [0,64)), O += P V
+//            with P read straight from TMEM (A-from-TMEM form) and V as an
+//            MN-major smem operand; O lives in TMEM cols [128,256)
+//   warps 2-5 softmax (one query row per thread = one TMEM lane): causal mask
+//            on the diagonal block only, online max with lazy rescaling
+//            (O is rescaled in TMEM only when the running max grows by more
+//            than 2^8), P = exp2(s*log2e/sqrt(d) - m), running sum; epilogue
+//            O / l -> bf16.
+// Two CTAs share an SM (256 TMEM columns and ~97 KB smem each), so one CTA's
+// softmax overlaps the other's MMAs.  GQA: q head h reads kv head h / group.
+#include <cuda_bf16.h>
+
+#include "sa_internal.h"
+#include "sa_ptx.cuh"
+
+namespace sa {
+namespace {
+
+constexpr int kThreads = 192;
+constexpr uint32_t kTileBytes = 128 * 128 * 2;
+constexpr uint32_t kBoxBytes = kTileBytes / 2;
+constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, false);
+constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 128, true);
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct __align__(8) K3Smem {
+  uint64_t q_full, k_full, k_empty, v_full, v_empty, s_full, p_full, o_full;
+  uint32_t tmem_base;
+};
+
+struct K3Params {
+  int S, Hq, nb, group, q_head0;
+  const int* kv_cnt;
+  const int* kv_idx;
+  const int* order;
+  __nv_bfloat16* out;
+  float* lse;
+  long long* touched;
+};
+
+__global__ void __launch_bounds__(kThreads, 2)
+    k3_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+          const __grid_constant__ CUtensorMap tm_v, const K3Params P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sQ = base;
+  unsigned char* sK = base + kTileBytes;
+  unsigned char* sV = base + 2 * kTileBytes;
+  K3Smem* sm = reinterpret_cast<K3Smem*>(base + 3 * kTileBytes);
+
+  const int item = P.order ? P.order[blockIdx.x] : (int)blockIdx.x;
+  const int h = item / P.nb, qb = item - h * P.nb;
+  const int n = P.kv_cnt[item];
+  const int* list = P.kv_idx + (size_t)h * tri(P.nb) + tri(qb);
+  const int kvh = kv_head_of(h, P.group, P.q_head0);
+  const int warp = warp_id();
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+    mbar_init(&sm->q_full, 1);
+    mbar_init(&sm->k_full, 1);
+    mbar_init(&sm->k_empty, 1);
+    mbar_init(&sm->v_full, 1);
+    mbar_init(&sm->v_empty, 1);
+    mbar_init(&sm->s_full, 1);
+    mbar_init(&sm->p_full, 128);
+    mbar_init(&sm->o_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(&sm->tmem_base, 256);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm->tmem_base;
+  const uint32_t tS = tmem, tO = tmem + 128;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t keep = policy_evict_last();
+      mbar_expect_tx(&sm->q_full, kTileBytes);
+      tma_load_3d(sQ, &tm_q, &sm->q_full, 0, qb * 128, h);
+      tma_load_3d(sQ + kBoxBytes, &tm_q, &sm->q_full, 64, qb * 128, h);
+      for (int j = 0; j < n; ++j) {
+        const int key0 = __ldg(list + j) * 128;
+        if (j >= 1) mbar_wait(&sm->k_empty, (j - 1) & 1);
+        mbar_expect_tx(&sm->k_full, kTileBytes);
+        tma_load_3d_hint(sK, &tm_k, &sm->k_full, 0, key0, kvh, keep);
+        tma_load_3d_hint(sK + kBoxBytes, &tm_k, &sm->k_full, 64, key0, kvh, keep);
+        if (j >= 1) mbar_wait(&sm->v_empty, (j - 1) & 1);
+        mbar_expect_tx(&sm->v_full, kTileBytes);
+        tma_load_3d_hint(sV, &tm_v, &sm->v_full, 0, key0, kvh, keep);
+        tma_load_3d_hint(sV + kBoxBytes, &tm_v, &sm->v_full, 64, key0, kvh, keep);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+    mbar_wait(&sm->q_full, 0);
+    for (int j = 0; j <= n; ++j) {
+      if (j >= 1) {
+        // O += P_{j-1} V_{j-1}
+        mbar_wait(&sm->p_full, (j - 1) & 1);
+        mbar_wait(&sm->v_full, (j - 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_ts(tO, tS + kk * 8, sdesc_sw128(v_addr + kk * 2048, kBoxBytes, 1024), kIdescPV,
+                    (j > 1 || kk > 0) ? 1u : 0u);
+          umma_commit(&sm->v_empty);
+          if (j == n) umma_commit(&sm->o_full);
+        }
+        __syncwarp();
+      }
+      if (j < n) {
+        mbar_wait(&sm->k_full, j & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
+            umma_ss(tS, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024),
+                    kIdescQK, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&sm->s_full);
+          umma_commit(&sm->k_empty);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    const int i = quad * 32 + lane_id();  // query row within the block
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const float sl2 = 1.4426950408889634f * 0.08838834764831845f;  // log2(e) / sqrt(128)
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < n; ++j) {
+      const int kb = __ldg(list + j);
+      const int lim = kb == qb ? i : 127;
+      mbar_wait(&sm->s_full, j & 1);
+      tc_fence_after();
+      float mx = -INFINITY;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(tS + lane_off + ch * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+          if (ch * 32 + t <= lim) mx = fmaxf(mx, __uint_as_float(r[t]));
+      }
+      const float mxs = mx * sl2;
+      // tcgen05.ld/st are warp-collective: take the rescale decision per warp
+      if (__any_sync(0xffffffffu, mxs > m_ref + kRescaleThreshold)) {
+        const float m_new = fmaxf(m_ref, mxs);
+        if (j > 0) {
+          const float f = ex2(m_ref - m_new);
+          l *= f;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t r[32];
+            tmem_ld32(tO + lane_off + ch * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int t = 0; t < 32; ++t) r[t] = __float_as_uint(__uint_as_float(r[t]) * f);
+            tmem_st32(tO + lane_off + ch * 32, r);
+          }
+        }
+        m_ref = m_new;
+      }
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(tS + lane_off + ch * 32, r);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const int c0 = ch * 32 + 2 * t;
+          const float p0 = c0 <= lim ? ex2(fmaf(__uint_as_float(r[2 * t]), sl2, -m_ref)) : 0.f;
+          const float p1 = c0 + 1 <= lim ? ex2(fmaf(__uint_as_float(r[2 * t + 1]), sl2, -m_ref)) : 0.f;
+          l += p0 + p1;
+          pk[t] = pack_bf16(p0, p1);
+        }
+        tmem_st16(tS + lane_off + ch * 16, pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&sm->p_full);
+    }
+    // epilogue: O / l -> bf16
+    mbar_wait(&sm->o_full, 0);
+    tc_fence_after();
+    const int row = qb * 128 + i;
+    const bool valid = row < P.S;
+    const float inv = 1.f / l;
+    __nv_bfloat16* dst = P.out + ((size_t)h * P.S + row) * 128;
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+      uint32_t r[32];
+      tmem_ld32(tO + lane_off + ch * 32, r);
+      tmem_ld_wait();
+      uint32_t pk[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        pk[t] = pack_bf16(__uint_as_float(r[2 * t]) * inv, __uint_as_float(r[2 * t + 1]) * inv);
+      if (valid) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + ch * 32);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) d4[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+      }
+    }
+    if (valid && P.lse) P.lse[(size_t)h * P.S + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
+    if (threadIdx.x == 64 && P.touched)
+      atomicAdd(reinterpret_cast<unsigned long long*>(P.touched + h), (unsigned long long)n);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+}  // namespace
+
+int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq, int Hkv, int group,
+                     int q_head0, const int* kv_cnt, const int* kv_idx, const int* order, void* out,
+                     float* lse, long long* touched, cudaStream_t st) {
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_bf16_hsd(&tq, q, Hq, S, 128) || !make_tmap_bf16_hsd(&tk, k, Hkv, S, 128) ||
+      !make_tmap_bf16_hsd(&tv, v, Hkv, S, 128))
+    return fail(SA_ERR_CUDA, "sparse_forward: cuTensorMapEncodeTiled failed");
+  K3Params P;
+  P.S = S;
+  P.Hq = Hq;
+  P.nb = ceil_div(S, 128);
+  P.group = group;
+  P.q_head0 = q_head0;
+  P.kv_cnt = kv_cnt;
+  P.kv_idx = kv_idx;
+  P.order = order;
+  P.out = static_cast<__nv_bfloat16*>(out);
+  P.lse = lse;
+  P.touched = touched;
+  const size_t smem = 3 * kTileBytes + sizeof(K3Smem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  if (touched) cudaMemsetAsync(touched, 0, sizeof(long long) * Hq, st);
+  k3_tc<<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P);
+  return check_launch("sparse_forward tcgen05");
+}
+
+}  // namespace sa

@@ -1,0 +1,320 @@
+// Stage 1, tensor-core mode: fused sampled-query attention + column / slash
+// block reduction on sm_100a (replaces sample_scores + block_reduce,
+// ref pkg/src/blocksift/sampler.py:135-191; math of core.py:110-154).
+//
+// One CTA = (q head h, chunk c, key-block split).  The chunk's 128 sampled
+// query rows (a possibly UNALIGNED window, sampler.py:103-117) are TMA-loaded
+// once; key tiles stream through a 2-stage TMA ring; S = Q K^T is computed by
+// tcgen05.mma into a double-buffered TMEM accumulator (2 x 128 columns) so
+// the MMA of tile j+1 overlaps the softmax of tile j.  Four softmax warps own
+// one sampled row each per thread (TMEM lane == row) and, per key block, emit
+// the row's running log2-max m and the two partial masses
+//     A = sum_{t <= r%128} exp2(s - m),   B = sum_{t > r%128} exp2(s - m)
+// (keys j = kb*128 + t, causal j <= r).  A lands in slash bin r//128 - kb and
+// B in r//128 - kb - 1, both in column bin kb.  The score matrix never leaves
+// TMEM/registers; the per-(row, block) partials (12 B per 128 keys) are the
+// only HBM traffic, and two tiny deterministic kernels normalise them with
+// the rows' global max / sum and fold the 128 rows into part3 (col + 3 slash
+// bins per key block), finished by the shared s1_finalize.
+#include <cuda_bf16.h>
+
+#include "sa_internal.h"
+#include "sa_ptx.cuh"
+
+namespace sa {
+namespace {
+
+constexpr int kThreads = 192;  // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 softmax
+constexpr int kStages = 2;
+constexpr uint32_t kTileBytes = 128 * 128 * 2;  // one 128 x 128 bf16 tile (two 64-col boxes)
+constexpr uint32_t kBoxBytes = kTileBytes / 2;
+constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, false);
+
+struct __align__(8) K1Smem {
+  uint64_t q_full;
+  uint64_t k_full[kStages];
+  uint64_t k_empty[kStages];
+  uint64_t s_full[2];
+  uint64_t s_empty[2];
+  uint32_t tmem_base;
+};
+
+struct K1Params {
+  Stage1Geom g;
+  const int* only;
+  int kb_per_cta;
+  float* pa;  // [Hq*cn][128][nb]
+  float* pb;
+  float* pm;
+};
+
+__global__ void __launch_bounds__(kThreads, 2)
+    k1_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+          const K1Params P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for the 128B-swizzled tiles
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sQ = base;                 // 32 KB
+  unsigned char* sK = base + kTileBytes;    // kStages x 32 KB
+  K1Smem* sm = reinterpret_cast<K1Smem*>(base + kTileBytes * (1 + kStages));
+
+  const Stage1Geom& g = P.g;
+  const int hc = blockIdx.y;
+  if (P.only && P.only[hc] == 0) return;
+  const int h = hc / g.cn, c = hc - h * g.cn;
+  int se, ss;
+  if (g.S < 128) {
+    ss = 0;
+    se = g.S;
+  } else {
+    se = (c + 1) * g.itv;
+    ss = se - 128;
+  }
+  const int nkb = (se + 127) / 128;
+  const int kb0 = blockIdx.x * P.kb_per_cta;
+  if (kb0 >= nkb) return;
+  const int n = min(P.kb_per_cta, nkb - kb0);
+  const int kvh = kv_head_of(h, g.group, g.q_head0);
+  const int warp = warp_id();
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_k);
+    mbar_init(&sm->q_full, 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&sm->k_full[i], 1);
+      mbar_init(&sm->k_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm->s_full[i], 1);
+      mbar_init(&sm->s_empty[i], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(&sm->tmem_base, 256);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm->tmem_base;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_expect_tx(&sm->q_full, kTileBytes);
+      tma_load_3d(sQ, &tm_q, &sm->q_full, 0, ss, h);
+      tma_load_3d(sQ + kBoxBytes, &tm_q, &sm->q_full, 64, ss, h);
+      for (int j = 0; j < n; ++j) {
+        const int st = j % kStages;
+        if (j >= kStages) mbar_wait(&sm->k_empty[st], ((j / kStages) - 1) & 1);
+        unsigned char* dst = sK + st * kTileBytes;
+        const int key0 = (kb0 + j) * 128;
+        mbar_expect_tx(&sm->k_full[st], kTileBytes);
+        tma_load_3d(dst, &tm_k, &sm->k_full[st], 0, key0, kvh);
+        tma_load_3d(dst + kBoxBytes, &tm_k, &sm->k_full[st], 64, key0, kvh);
+      }
+    }
+  } else if (warp == 1) {
+    mbar_wait(&sm->q_full, 0);
+    const uint32_t q_addr = smem_u32(sQ);
+    for (int j = 0; j < n; ++j) {
+      const int st = j % kStages, buf = j & 1;
+      mbar_wait(&sm->k_full[st], (j / kStages) & 1);
+      if (j >= 2) mbar_wait(&sm->s_empty[buf], ((j >> 1) - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t k_addr = smem_u32(sK + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
+          umma_ss(tmem + buf * 128, sdesc_sw128(q_addr + off, 16, 1024),
+                  sdesc_sw128(k_addr + off, 16, 1024), kIdescQK, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&sm->s_full[buf]);
+        umma_commit(&sm->k_empty[st]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // softmax warps: TMEM lane quadrant = warp % 4
+    const int quad = warp & 3;
+    const int rl = quad * 32 + lane_id();       // row within the window
+    const int row = ss + rl;                    // global query position
+    const bool valid = row < se;
+    const int rho = row & 127;
+    const float sl2 = 1.4426950408889634f / sqrtf((float)g.d);
+    float m_run = -INFINITY;
+    const size_t prow = ((size_t)hc * 128 + rl) * g.nb;
+    for (int j = 0; j < n; ++j) {
+      const int buf = j & 1;
+      const int kb = kb0 + j;
+      mbar_wait(&sm->s_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * 128;
+      const int lim = row - kb * 128;  // keys t <= lim are causal
+      float mx = -INFINITY;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(taddr + ch * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float x = __uint_as_float(r[i]);
+          if (ch * 32 + i <= lim) mx = fmaxf(mx, x);
+        }
+      }
+      const float m_new = fmaxf(m_run, mx * sl2);
+      float a = 0.f, b = 0.f;
+      // warp-collective TMEM loads stay outside any per-row condition
+      const int lim_e = m_new == -INFINITY ? -1 : lim;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(taddr + ch * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int t = ch * 32 + i;
+          const float p = t <= lim_e ? ex2(fmaf(__uint_as_float(r[i]), sl2, -m_new)) : 0.f;
+          if (t <= rho) a += p; else b += p;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm->s_empty[buf]);
+      if (valid) {
+        P.pa[prow + kb] = a;
+        P.pb[prow + kb] = b;
+        P.pm[prow + kb] = m_new;
+      }
+      m_run = m_new;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+// Per sampled row: global log2-max M and normaliser L over all key blocks.
+// One warp per row, lanes stride the key blocks (coalesced); fixed-order
+// shuffle tree -> deterministic.
+__global__ void k1_rowfin(Stage1Geom g, const int* __restrict__ only, const float* __restrict__ pa,
+                          const float* __restrict__ pb, const float* __restrict__ pm,
+                          double* __restrict__ rowstat) {
+  const int hc = blockIdx.x;
+  if (only && only[hc] == 0) return;
+  const int c = hc % g.cn;
+  const int se = g.S < 128 ? g.S : (c + 1) * g.itv;
+  const int nr = g.S < 128 ? g.S : 128;
+  const int nkb = (se + 127) / 128;
+  const int lane = threadIdx.x & 31;
+  for (int rl = threadIdx.x >> 5; rl < nr; rl += blockDim.x >> 5) {
+    const size_t o = ((size_t)hc * 128 + rl) * g.nb;
+    float mx = -INFINITY;
+    for (int kb = lane; kb < nkb; kb += 32) mx = fmaxf(mx, pm[o + kb]);
+    for (int s = 16; s > 0; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+    double L = 0.0;
+    for (int kb = lane; kb < nkb; kb += 32) {
+      const float m = pm[o + kb];
+      if (m != -INFINITY) L += ((double)pa[o + kb] + (double)pb[o + kb]) * exp2((double)m - (double)mx);
+    }
+    for (int s = 16; s > 0; s >>= 1) L += __shfl_xor_sync(0xffffffffu, L, s);
+    if (lane == 0) {
+      rowstat[((size_t)hc * 128 + rl) * 2] = mx;
+      rowstat[((size_t)hc * 128 + rl) * 2 + 1] = L;
+    }
+  }
+}
+
+// Per key block: fold the 128 rows' normalised partial masses into part3.
+__global__ void k1_fold(Stage1Geom g, const int* __restrict__ only, const float* __restrict__ pa,
+                        const float* __restrict__ pb, const float* __restrict__ pm,
+                        const double* __restrict__ rowstat, double* __restrict__ part3) {
+  __shared__ double s_w[128][2];  // (M, 1/L) per row
+  const int hc = blockIdx.y;
+  if (only && only[hc] == 0) return;
+  const int c = hc % g.cn;
+  int ss, se;
+  if (g.S < 128) {
+    ss = 0;
+    se = g.S;
+  } else {
+    se = (c + 1) * g.itv;
+    ss = se - 128;
+  }
+  const int nr = se - ss;
+  const int nkb = (se + 127) / 128;
+  for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+    s_w[r][0] = rowstat[((size_t)hc * 128 + r) * 2];
+    s_w[r][1] = 1.0 / rowstat[((size_t)hc * 128 + r) * 2 + 1];
+  }
+  __syncthreads();
+  const int kb = blockIdx.x * blockDim.x + threadIdx.x;
+  if (kb >= g.nb) return;
+  double* out = part3 + ((size_t)hc * g.nb + kb) * 4;
+  if (kb >= nkb) {
+    out[0] = out[1] = out[2] = out[3] = 0.0;
+    return;
+  }
+  const int b0 = ss / 128;
+  double s4[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int r = 0; r < nr; ++r) {
+    const size_t o = ((size_t)hc * 128 + r) * g.nb + kb;
+    const float m = pm[o];
+    if (m == -INFINITY) continue;
+    const double w = exp2((double)m - s_w[r][0]) * s_w[r][1];
+    const double a = (double)pa[o] * w, b = (double)pb[o] * w;
+    const int slot_a = (ss + r) / 128 - b0 + 1;  // bin r//128 - kb  -> slot relative to X-1
+    s4[0] += a + b;
+    s4[1 + slot_a] += a;
+    s4[slot_a] += b;  // bin r//128 - kb - 1
+  }
+  out[0] = s4[0];
+  out[1] = s4[1];
+  out[2] = s4[2];
+  out[3] = s4[3];
+}
+
+}  // namespace
+
+int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const int* only, char* ws,
+                     const Workspace& L, double* col, double* slash, cudaStream_t st) {
+  CUtensorMap tq, tk;
+  if (!make_tmap_bf16_hsd(&tq, q, g.Hq, g.S, 128) || !make_tmap_bf16_hsd(&tk, k, g.Hkv, g.S, 128))
+    return fail(SA_ERR_CUDA, "stage1: cuTensorMapEncodeTiled failed");
+  const size_t plane = (size_t)g.Hq * g.cn * 128 * g.nb;
+  K1Params P;
+  P.g = g;
+  P.only = only;
+  P.pa = reinterpret_cast<float*>(ws + L.tc_part);
+  P.pb = P.pa + plane;
+  P.pm = P.pb + plane;
+  // split the key range so the grid covers the SMs a few times over
+  const long long total_kb = (long long)g.Hq * g.cn * g.nb;
+  int kpc = (int)std::max<long long>(4, std::min<long long>(64, total_kb / (148LL * 2 * 4)));
+  P.kb_per_cta = kpc;
+  const int nsplit = ceil_div(g.nb, kpc);
+  const size_t smem = kTileBytes * (1 + kStages) + sizeof(K1Smem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k1_tc<<<dim3(nsplit, g.Hq * g.cn), kThreads, smem, st>>>(tq, tk, P);
+  if (int e = check_launch("stage1 tcgen05")) return e;
+  double* rowstat = reinterpret_cast<double*>(ws + L.rowstat);
+  double* part3 = reinterpret_cast<double*>(ws + L.part3);
+  k1_rowfin<<<g.Hq * g.cn, 256, 0, st>>>(g, only, P.pa, P.pb, P.pm, rowstat);
+  if (int e = check_launch("stage1 rowfin")) return e;
+  k1_fold<<<dim3(ceil_div(g.nb, 128), g.Hq * g.cn), 128, 0, st>>>(g, only, P.pa, P.pb, P.pm, rowstat,
+                                                                  part3);
+  if (int e = check_launch("stage1 fold")) return e;
+  return launch_stage1_finalize(g, only, part3, col, slash, st);
+}
+
+}  // namespace sa

@@ -1,0 +1,320 @@
+// Stage 2: minimal-quota selection and block-mask assembly.
+//
+// k2_select  replaces find_k + arg_topk (ref pkg/src/blocksift/filtering.py:30-62)
+//            for every (head, chunk, direction) of select_and_merge (:245-255):
+//            block-wide bitonic sort on (score desc, index asc), the reference's
+//            SEQUENTIAL fp64 cumulative sum (bit-exact with np.cumsum), first
+//            index with cum >= alpha * cum[-1], then the picked index set
+//            compacted in ascending order.  Optional selection guard: flags a
+//            (head, chunk) whose alpha cut or boundary tie gap lies within
+//            eps * total of a decision.
+// k2_merge   replaces merge_index (:198-230): one warp per (head, query block)
+//            builds the union of column picks (kb <= qb), slash picks
+//            ({qb-ob-1, qb-ob} clipped to [0, qb]) of the 1-2 chunks whose
+//            region covers qb, and the diagonal, as an ascending list.
+// k2_full    dense causal mask (the dense comparison row).
+// k2_sched   longest-first order of (head, query block) work items.
+#include <algorithm>
+
+#include "sa_internal.h"
+
+namespace sa {
+namespace {
+
+constexpr int kSelThreads = 1024;
+
+__device__ __forceinline__ bool before(unsigned long long ka, int ia, unsigned long long kb_, int ib) {
+  return ka > kb_ || (ka == kb_ && ia < ib);
+}
+
+__global__ void __launch_bounds__(kSelThreads)
+    k2_select(const double* __restrict__ col, const double* __restrict__ slash, int cn, int nb,
+              int npow2, double alpha_c, double alpha_s, double eps, int* __restrict__ flags,
+              const int* __restrict__ only, const int* __restrict__ k_in, int* __restrict__ k_out,
+              int* __restrict__ idx_out) {
+  extern __shared__ unsigned char smem_raw[];
+  const int dir = blockIdx.x, hc = blockIdx.y;
+  if (only && only[hc] == 0) return;
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);  // [npow2]
+  double* cum = reinterpret_cast<double*>(key + npow2);                      // [npow2]
+  int* idx = reinterpret_cast<int*>(cum + npow2);                            // [npow2]
+  unsigned char* mark = reinterpret_cast<unsigned char*>(idx + npow2);       // [npow2]
+  __shared__ int s_k;
+  __shared__ int s_warp[32];
+
+  const double* s = (dir == 0 ? col : slash) + (size_t)hc * nb;
+  const double alpha = dir == 0 ? alpha_c : alpha_s;
+  for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+    double v = i < nb ? s[i] : 0.0;
+    // scores are nonnegative; fold -0.0 onto +0.0 so bit order == value order
+    key[i] = v > 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
+    idx[i] = i < nb ? i : 0x7fffffff;
+    mark[i] = 0;
+  }
+  __syncthreads();
+  // bitonic sort into "before" order (descending score, ascending index)
+  for (int size = 2; size <= npow2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (npow2 >> 1); t += blockDim.x) {
+        const int lo = 2 * stride * (t / stride) + (t % stride);
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const unsigned long long ka = key[lo], kb_ = key[hi];
+        const int ia = idx[lo], ib = idx[hi];
+        const bool swap = up ? before(kb_, ib, ka, ia) : before(ka, ia, kb_, ib);
+        if (swap) {
+          key[lo] = kb_;
+          key[hi] = ka;
+          idx[lo] = ib;
+          idx[hi] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // sequential fp64 cumulative sum in sorted order (np.cumsum semantics)
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    int i = 0;
+    for (; i < nb; ++i) {
+      const unsigned long long kk = key[i];
+      if (kk == 0ull) break;  // the zero tail leaves the sum unchanged
+      acc += __longlong_as_double((long long)kk);
+      cum[i] = acc;
+    }
+    for (; i < nb; ++i) cum[i] = acc;
+  }
+  __syncthreads();
+  const double total = cum[nb - 1];
+  const double target = alpha * total;
+  // k = searchsorted(cum, target, 'left') + 1 = #(cum < target) + 1
+  int cnt = 0;
+  if (target > 0.0)
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) cnt += cum[i] < target ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s_warp[w];
+    int k = target > 0.0 ? tot + 1 : 0;
+    if (k_in) k = min(max(k_in[hc * 2 + dir], 0), nb);
+    s_k = k;
+    k_out[hc * 2 + dir] = k;
+    if (eps > 0.0 && k > 0 && flags && !k_in) {
+      const double E = eps * total;
+      bool close = (cum[k - 1] - target) < E;
+      if (k >= 2 && (target - cum[k - 2]) < E) close = true;
+      if (k < nb) {
+        const double a = __longlong_as_double((long long)key[k - 1]);
+        const double b = __longlong_as_double((long long)key[k]);
+        if (a - b < E) close = true;
+      }
+      if (close) atomicOr(flags + hc, 1);
+    }
+  }
+  __syncthreads();
+  const int k = s_k;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) mark[idx[i]] = 1;
+  __syncthreads();
+  // ascending compaction of the picked indices: each thread owns a contiguous run
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int a0 = threadIdx.x * per, a1 = min(nb, a0 + per);
+  int local = 0;
+  for (int i = a0; i < a1; ++i) local += mark[i];
+  // block exclusive scan of `local`
+  int incl = local;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  __syncthreads();
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int v = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    s_warp[lane] = v;
+  }
+  __syncthreads();
+  int pos = incl - local + (wid > 0 ? s_warp[wid - 1] : 0);
+  int* dst = idx_out + ((size_t)hc * 2 + dir) * nb;
+  for (int i = a0; i < a1; ++i)
+    if (mark[i]) dst[pos++] = i;
+}
+
+constexpr int kMergeWarps = 8;
+
+__global__ void __launch_bounds__(kMergeWarps * 32)
+    k2_merge(const int* __restrict__ k_sel, const int* __restrict__ idx_sel, int Hq, int cn, int nb,
+             int S, int blk, int itv, int sink_blocks, int local_blocks, int* __restrict__ kv_cnt,
+             int* __restrict__ kv_idx, long long* __restrict__ active_blocks,
+             long long* __restrict__ active_entries) {
+  extern __shared__ unsigned int bits_all[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long item = (long long)blockIdx.x * kMergeWarps + wid;
+  if (item >= (long long)Hq * nb) return;
+  const int h = (int)(item / nb), qb = (int)(item - (long long)h * nb);
+  const int nwords = (nb + 31) >> 5;
+  unsigned int* bits = bits_all + wid * nwords;
+  const int w_used = (qb >> 5) + 1;
+  for (int w = lane; w < w_used; w += 32) bits[w] = 0u;
+  __syncwarp();
+  const int row0 = qb * blk, row1 = min(row0 + blk, S) - 1;
+  const int c_first = min(cn - 1, row0 / itv), c_last = min(cn - 1, row1 / itv);
+  for (int c = c_first; c <= c_last; ++c) {
+    const int hc = h * cn + c;
+    const int kc = k_sel[hc * 2], ks = k_sel[hc * 2 + 1];
+    const int* ic = idx_sel + ((size_t)hc * 2) * nb;
+    const int* is = ic + nb;
+    for (int i = lane; i < kc; i += 32) {
+      const int kb = ic[i];
+      if (kb <= qb) atomicOr(bits + (kb >> 5), 1u << (kb & 31));
+    }
+    for (int i = lane; i < ks; i += 32) {
+      const int ob = is[i];
+      const int kb1 = qb - ob - 1, kb2 = qb - ob;
+      if (kb1 >= 0) atomicOr(bits + (kb1 >> 5), 1u << (kb1 & 31));
+      if (kb2 >= 0) atomicOr(bits + (kb2 >> 5), 1u << (kb2 & 31));
+    }
+  }
+  if (lane == 0) atomicOr(bits + (qb >> 5), 1u << (qb & 31));
+  // optional forced sink / local-window blocks (defaults 0 / 1 add nothing)
+  for (int kb = lane; kb < min(sink_blocks, qb + 1); kb += 32) atomicOr(bits + (kb >> 5), 1u << (kb & 31));
+  for (int kb = max(0, qb - local_blocks + 1) + lane; kb < qb; kb += 32)
+    atomicOr(bits + (kb >> 5), 1u << (kb & 31));
+  __syncwarp();
+  int* dst = kv_idx + (size_t)h * tri(nb) + tri(qb);
+  int off = 0;
+  for (int w0 = 0; w0 < w_used; w0 += 32) {
+    const int w = w0 + lane;
+    unsigned int word = w < w_used ? bits[w] : 0u;
+    const int pc = __popc(word);
+    int incl = pc;
+    for (int o = 1; o < 32; o <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int pos = off + incl - pc;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      dst[pos++] = (w << 5) + b;
+      word &= word - 1;
+    }
+    off += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) {
+    kv_cnt[(size_t)h * nb + qb] = off;
+    if (active_blocks) atomicAdd(reinterpret_cast<unsigned long long*>(active_blocks + h), (unsigned long long)off);
+    if (active_entries) {
+      const long long m = min(blk, S - row0);
+      const long long e = (long long)(off - 1) * m * blk + m * (m + 1) / 2;
+      atomicAdd(reinterpret_cast<unsigned long long*>(active_entries + h), (unsigned long long)e);
+    }
+  }
+}
+
+__global__ void k2_full(int Hq, int nb, int* __restrict__ kv_cnt, int* __restrict__ kv_idx) {
+  const long long item = blockIdx.x;
+  const int h = (int)(item / nb), qb = (int)(item - (long long)h * nb);
+  int* dst = kv_idx + (size_t)h * tri(nb) + tri(qb);
+  for (int i = threadIdx.x; i <= qb; i += blockDim.x) dst[i] = i;
+  if (threadIdx.x == 0) kv_cnt[item] = qb + 1;
+}
+
+// counting sort of work items by descending block count (single CTA)
+__global__ void __launch_bounds__(1024) k2_sched(const int* __restrict__ kv_cnt, int n_items, int nb,
+                                                 int* __restrict__ order) {
+  extern __shared__ int hist[];  // [nb + 2]
+  for (int i = threadIdx.x; i < nb + 2; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_items; i += blockDim.x) {
+    int c = min(max(kv_cnt[i], 0), nb);
+    atomicAdd(hist + c, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;  // descending: bin nb first
+    for (int c = nb; c >= 0; --c) {
+      const int v = hist[c];
+      hist[c] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_items; i += blockDim.x) {
+    int c = min(max(kv_cnt[i], 0), nb);
+    const int slot = atomicAdd(hist + c, 1);
+    order[slot] = i;
+  }
+}
+
+__global__ void k_check_finite_f32(const float* __restrict__ x, long long n, int* flag) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) *flag = 1;
+}
+__global__ void k_check_finite_bf16(const unsigned short* __restrict__ x, long long n, int* flag) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if ((x[i] & 0x7f80u) == 0x7f80u) *flag = 1;
+}
+
+}  // namespace
+
+int launch_select(const double* col, const double* slash, int Hq, int cn, int nb, double ac,
+                  double as, double eps, int* flags, const int* only, const int* k_in, int* k_out,
+                  int* idx_out, cudaStream_t st) {
+  int npow2 = 1;
+  while (npow2 < nb) npow2 <<= 1;
+  const size_t smem = (size_t)npow2 * (8 + 8 + 4 + 1);
+  if (smem > 220 * 1024) return fail(SA_ERR_UNSUPPORTED, "sa_select: too many blocks (nb > 8192)");
+  cudaFuncSetAttribute(k2_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int threads = npow2 >= 2048 ? 1024 : (npow2 >= 64 ? npow2 / 2 : 32);
+  k2_select<<<dim3(2, Hq * cn), threads, smem, st>>>(col, slash, cn, nb, npow2, ac, as, eps, flags,
+                                                     only, k_in, k_out, idx_out);
+  return check_launch("sa_select");
+}
+
+int launch_merge(const int* k_sel, const int* idx_sel, int Hq, int cn, int nb, int S, int blk,
+                 int itv, int sink_blocks, int local_blocks, int* kv_cnt, int* kv_idx,
+                 long long* ab, long long* ae, cudaStream_t st) {
+  const long long items = (long long)Hq * nb;
+  const int nwords = (nb + 31) / 32;
+  const size_t smem = (size_t)kMergeWarps * nwords * 4;
+  const int grid = (int)((items + kMergeWarps - 1) / kMergeWarps);
+  if (ab) cudaMemsetAsync(ab, 0, sizeof(long long) * Hq, st);
+  if (ae) cudaMemsetAsync(ae, 0, sizeof(long long) * Hq, st);
+  k2_merge<<<grid, kMergeWarps * 32, smem, st>>>(k_sel, idx_sel, Hq, cn, nb, S, blk, itv,
+                                                   sink_blocks, local_blocks, kv_cnt, kv_idx, ab, ae);
+  return check_launch("sa_merge");
+}
+
+int launch_full(int Hq, int nb, int* kv_cnt, int* kv_idx, cudaStream_t st) {
+  k2_full<<<Hq * nb, 128, 0, st>>>(Hq, nb, kv_cnt, kv_idx);
+  return check_launch("sa_full_mask");
+}
+
+int launch_sched(const int* kv_cnt, int n_items, int nb, int* order, cudaStream_t st) {
+  const size_t smem = (size_t)(nb + 2) * 4;
+  if (smem > 200 * 1024) return fail(SA_ERR_UNSUPPORTED, "sa_schedule: nb too large");
+  cudaFuncSetAttribute(k2_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k2_sched<<<1, 1024, smem, st>>>(kv_cnt, n_items, nb, order);
+  return check_launch("sa_schedule");
+}
+
+int launch_check_finite(const void* x, int dtype, long long n, int* flag, cudaStream_t st) {
+  if (n <= 0) return SA_OK;
+  const int grid = (int)std::min<long long>(148LL * 8, (n + 255) / 256);
+  if (dtype == SA_FP32)
+    k_check_finite_f32<<<grid, 256, 0, st>>>(static_cast<const float*>(x), n, flag);
+  else
+    k_check_finite_bf16<<<grid, 256, 0, st>>>(static_cast<const unsigned short*>(x), n, flag);
+  return check_launch("sa_check_finite");
+}
+
+}  // namespace sa

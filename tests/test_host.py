@@ -1,0 +1,79 @@
+"""CPU-side checks: the C-ABI library loads and exports every declared
+symbol, and the host integer logic (config, plan) matches the pinned oracle."""
+
+import os
+import re
+
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import paper_2406_15486_b200 as sa
+from oracle import blocksift_port as O
+from paper_2406_15486_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "sampleattn.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|long long|const char\*)\s+(sa_\w+)\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 10
+    for name in syms:
+        assert hasattr(lib, name), name
+    assert sorted(_lib.exported_symbols()) == syms
+    assert lib.sa_version() >= 100
+
+
+def test_workspace_bytes_positive():
+    lib = _lib.load()
+    assert lib.sa_workspace_bytes(131072, 32, 2, 128, 128, 1, _lib.SA_BF16) > 0
+    assert lib.sa_workspace_bytes(0, 32, 2, 128, 128, 1, _lib.SA_BF16) == 0
+
+
+def test_config_defaults_and_validation():
+    cfg = sa.SparseConfig()
+    assert (cfg.alpha_c, cfg.alpha_s, cfg.chunk_n, cfg.blk) == (0.95, 0.95, 1, 128)
+    for kw in ({"alpha_c": -0.1}, {"alpha_s": 1.5}, {"chunk_n": 0}, {"blk": 0}):
+        with pytest.raises(sa.InputError):
+            sa.SparseConfig(**kw)
+
+
+def test_resolve_config_shorthands():
+    c = sa.resolve_config(98304, alpha=0.9, sample_ratio=0.02)
+    assert (c.alpha_c, c.alpha_s, c.chunk_n) == (0.9, 0.9, 15)
+    c = sa.resolve_config(4096, alpha=0.95, sample_ratio=0.05)
+    assert c.chunk_n == 2
+    c = sa.resolve_config(4096, alpha=0.9, alpha_s=0.98)
+    assert (c.alpha_c, c.alpha_s) == (0.9, 0.98)
+    with pytest.raises(sa.InputError):
+        sa.resolve_config(4096, chunk_n=2, sample_ratio=0.1)
+
+
+@given(S=st.integers(1, 5000), chunk_n=st.integers(1, 16), blk=st.integers(1, 512))
+@settings(max_examples=300, deadline=None)
+def test_plan_matches_oracle(S, chunk_n, blk):
+    p = sa.plan_chunks(S, sa.SparseConfig(chunk_n=chunk_n, blk=blk))
+    o = O.plan_chunks(S, chunk_n, blk)
+    assert (p.chunk_n, p.itv) == (o.chunk_n, o.itv)
+    assert [(c.sample_start, c.sample_end, c.region_start, c.region_end) for c in p.chunks] == list(o.windows)
+
+
+def test_plan_kats():
+    p = sa.plan_chunks(300, sa.SparseConfig(chunk_n=4, blk=128))
+    assert p.chunk_n == 2 and p.itv == 150
+    assert [(c.sample_start, c.sample_end) for c in p.chunks] == [(22, 150), (172, 300)]
+    assert sa.plan_chunks(65536, sa.SparseConfig(chunk_n=2)).sampled_rows() == 256
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2406_15486_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            src = open(os.path.join(pkg, fn)).read()
+            assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\S+)", src, re.M), fn
