@@ -1,0 +1,441 @@
+"""Benchmark: SampleAttention sparse prefill at 128K (ChatGLM3-6B attention
+shape: 32 q heads, 2 KV heads, d = 128), alpha = 0.95, one sampled window.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line (rank 0).  A "step" is one full prefill-attention pass of the
+hot path (stage 1 sampled scores -> stage 2 selection/merge -> stage 3 sparse
+attention) over every q head of the job.  N > 1 (torchrun) shards q heads
+across ranks (each rank owns whole heads and the KV heads they read; no
+collective on the data path); the job's total work is fixed, so scaling is
+"strong".
+
+value  = dense-equivalent causal FLOPs of the job (4*d*sum_{kb<=qb} m*n,
+         ref executor.py:65) / device time per step (max over ranks): the
+         reference's "effective TFLOP/s".  Inputs resident in HBM; L2 flushed
+         between timed steps.
+e2e    = the same metric through the public API from pinned host buffers
+         (q/k/v H2D + sample_attention + output D2H inside the timed region).
+roofline: stage-3 kernel, kept FLOPs (4*d*sum_active m*n, executor.py:66)
+         per launch / its CUDA-event duration, against the measured bf16 peak.
+cpu_baseline: the CPU oracle (numpy port of the reference path) on a bounded
+         sample of one head, extrapolated per head.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (S, Hq, Hkv, alpha, chunk_n, description)
+    "c3": (131072, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 128K, bf16, alpha 0.95, chunk_n 1"),
+    "c2": (32768, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 32K, bf16, alpha 0.95, chunk_n 1"),
+    "c4": (98304, 32, 8, 0.95, 15, "InternLM2-7B attention shape, seq 96K, bf16, alpha 0.95, 2% sampling"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dense_flops(S: int, d: int, blk: int = 128) -> int:
+    """ref executor.py:65 for one head: 4*d*sum over causal block pairs of m*n."""
+    nb = -(-S // blk)
+    sizes = [min(blk, S - i * blk) for i in range(nb)]
+    return 4 * d * sum(sizes[q] * (q * blk + sizes[q]) for q in range(nb))
+
+
+# ------------------------------------------------------------------ CPU side
+def cpu_sample(q, k, v, alpha, chunk_n, blk=128, n_qblocks=8, seed=0):
+    """Time the CPU oracle on one head: stage 1+2 in full, stage 3 on a seeded
+    sample of query blocks; returns per-head seconds (extrapolated) and detail."""
+    import numpy as np
+    from oracle import blocksift_port as O
+
+    S, d = q.shape
+    t0 = time.perf_counter()
+    plan = O.plan_chunks(S, chunk_n, blk)
+    samples = O.sampled_probs(q, k, plan)
+    cols, slashes, _ = O.block_reduce(samples, S, blk)
+    t1 = time.perf_counter()
+    sel, grid = O.select_and_merge(cols, slashes, plan, alpha, alpha)
+    t2 = time.perf_counter()
+    nb = grid.shape[0]
+    rng = np.random.default_rng(seed)
+    qbs = sorted(rng.choice(nb, size=min(n_qblocks, nb), replace=False).tolist())
+    blocks = 0
+    t3 = time.perf_counter()
+    for qb in qbs:  # stage 3 restricted to the sampled query blocks (same recurrence)
+        _sparse_rows(O, q, k, v, grid, qb, blk)
+        blocks += int(grid[qb].sum())
+    t4 = time.perf_counter()
+    total_blocks = int(grid.sum())
+    t_stage3 = (t4 - t3) * total_blocks / max(1, blocks)
+    return {"t_stage1": t1 - t0, "t_stage2": t2 - t1, "t_stage3_extrapolated": t_stage3,
+            "t_head": (t1 - t0) + (t2 - t1) + t_stage3, "sampled_qblocks": len(qbs),
+            "sampled_blocks": blocks, "head_blocks": total_blocks, "density": total_blocks / (nb * (nb + 1) / 2)}
+
+
+def _sparse_rows(O, q, k, v, grid, qb, blk):
+    import numpy as np
+
+    S, d = q.shape
+    a, b = qb * blk, min((qb + 1) * blk, S)
+    qs = q[a:b] * (1.0 / np.sqrt(d))
+    m = np.full(b - a, -np.inf)
+    l = np.zeros(b - a)
+    acc = np.zeros((b - a, d))
+    for kb in np.flatnonzero(grid[qb]):
+        c0, c1 = kb * blk, min((kb + 1) * blk, S)
+        z = qs @ k[c0:c1].T
+        if kb == qb:
+            z[np.arange(c0, c1)[None, :] > np.arange(a, b)[:, None]] = -np.inf
+        mn = np.maximum(m, z.max(axis=1))
+        corr = np.exp(m - mn)
+        pz = np.exp(z - mn[:, None])
+        l = corr * l + pz.sum(axis=1)
+        acc = acc * corr[:, None] + pz @ v[c0:c1]
+        m = mn
+    return acc / l[:, None]
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--alpha", type=float, default=None)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--guard", default="auto", choices=["auto", "always", "never"])
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    S, Hq, Hkv, alpha, chunk_n, desc = CONFIGS[args.config]
+    if args.alpha is not None:
+        alpha = args.alpha
+    d = 128
+    workload = {"workload": desc, "S": S, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d, "alpha": alpha,
+                "chunk_n": chunk_n, "blk": 128, "parallelism": f"heads/{world}", "l2": "flushed between steps"}
+
+    if args.impl == "reference":
+        return run_reference(args, rank, S, Hq, Hkv, d, alpha, chunk_n, workload)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2406_15486_b200 as sa
+    from paper_2406_15486_b200 import _lib, synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if Hq % world:
+        raise SystemExit(f"{Hq} heads do not shard over {world} ranks")
+    per = Hq // world
+    my_heads = list(range(rank * per, (rank + 1) * per))
+    group = Hq // Hkv
+    q, k, v, kv_heads = synth.make_inputs(S, Hq, Hkv, d, seed=args.seed, heads=my_heads, device=dev)
+    q_head0 = my_heads[0]
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    out = torch.empty_like(q)
+
+    def step(timings=False):
+        return sa.sample_attention(q, k, v, alpha=alpha, chunk_n=chunk_n, guard=args.guard, timings=timings,
+                                   q_head0=q_head0, group=group, out=out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # ---- timed region (device-resident inputs)
+    step_ms, k3_ms, s1_ms, s2_ms = [], [], [], []
+    launches0 = _lib.launch_count()
+    barrier()
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            o, res = step(timings=True)
+            e1.record()
+            torch.cuda.synchronize(dev)
+            step_ms.append(e0.elapsed_time(e1))
+            st = res.stage_ms()
+            k3_ms.append(st["stage3_ms"])
+            s1_ms.append(st["stage1_ms"])
+            s2_ms.append(st["stage2_ms"])
+    barrier()
+    launches = _lib.launch_count() - launches0
+    t_step = sum(step_ms) / len(step_ms)
+    t_local = torch.tensor([t_step], device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    t_max = float(t_local.item())
+
+    # ---- work accounting (after timing; host syncs allowed)
+    mask = res.mask
+    flop = sa.flop_accounting(mask, S, d)
+    kept = flop.estimated_flops_sparse
+    dense_job = dense_flops(S, d) * Hq
+    value = dense_job / (t_max * 1e-3) / 1e12
+    t_k3 = sum(k3_ms) / len(k3_ms)
+    pk, pk_kind = peaks()
+    achieved = kept / (t_k3 * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k3_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    roof = {"bound": "tensor", "kernel": "k3_tc (stage-3 sparse prefill)", "achieved": round(achieved, 2),
+            "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": round(achieved / pk["bf16_tflops"], 4),
+            "frac_of_sustained": round(achieved / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]), 4),
+            "peak_source": pk_kind, "traffic": traffic,
+            "flops_per_launch": kept, "launch_ms": round(t_k3, 3)}
+
+    extra = {"stage_ms": {"stage1": round(sum(s1_ms) / len(s1_ms), 3), "stage2": round(sum(s2_ms) / len(s2_ms), 3),
+                          "stage3": round(t_k3, 3)},
+             "filtering_overhead": round(1 - t_k3 / t_step, 4),
+             "block_density": round(flop.block_density, 4),
+             "rescored_pairs": res.n_rescored(),
+             "kept_tflop": round(kept / 1e12, 3), "dense_tflop": round(dense_job / world / 1e12, 3)}
+
+    # ---- dense comparison rows (same GPU, same inputs)
+    if not args.no_dense and rank == 0:
+        extra["dense"] = dense_rows(sa, q, k, v, group, dense_job / world, flush)
+        best = min(v_["ms"] for v_ in extra["dense"].values() if v_.get("ms"))
+        extra["speedup_vs_fastest_dense"] = round(best / t_step, 3)
+
+    # ---- end to end from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(sa, q, k, v, alpha, chunk_n, group, q_head0, args, dev, world, dense_job)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(q, k, v, kv_heads, group, alpha, chunk_n, S, d)
+
+    if rank == 0:
+        line = {"metric": "sparse prefill attention eff. TFLOP/s at 128K (ChatGLM3-6B shape, alpha=0.95)"
+                if args.config == "c3" else f"sparse prefill attention eff. TFLOP/s ({args.config})",
+                "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(t_max, 3), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (seeded GPU generator: Zipf column sinks + local band + slash band + noise)",
+                "config": workload, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk.summary(), **extra}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def dense_rows(sa, q, k, v, group, flops, flush):
+    import torch
+
+    rows = {}
+
+    def timeit(fn, reps=2):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return min(ts)
+
+    o = torch.empty_like(q)
+    ms = timeit(lambda: sa.dense_attention(q, k, v, out=o, group=group))
+    rows["ours_dense_k3"] = {"ms": round(ms, 3), "tflops": round(flops / ms / 1e9, 1)}
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+
+        qq, kk, vv = q[None], k[None], v[None]
+        with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+            ms = timeit(lambda: torch.nn.functional.scaled_dot_product_attention(qq, kk, vv, is_causal=True,
+                                                                                 enable_gqa=True))
+        rows["cudnn_sdpa"] = {"ms": round(ms, 3), "tflops": round(flops / ms / 1e9, 1)}
+    except Exception as e:  # pragma: no cover - depends on the box
+        rows["cudnn_sdpa"] = {"error": str(e)[:200]}
+    try:
+        from flash_attn import flash_attn_func
+
+        qf, kf, vf = (t.transpose(0, 1)[None] for t in (q, k, v))  # [1, S, H, d]
+        ms = timeit(lambda: flash_attn_func(qf, kf, vf, causal=True))
+        rows["flash_attn2"] = {"ms": round(ms, 3), "tflops": round(flops / ms / 1e9, 1)}
+    except Exception as e:  # pragma: no cover
+        rows["flash_attn2"] = {"error": str(e)[:200]}
+    return rows
+
+
+def e2e_run(sa, q, k, v, alpha, chunk_n, group, q_head0, args, dev, world, dense_job):
+    import torch
+
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    ho = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+    bi = sum(t.numel() * t.element_size() for t in (hq, hk, hv))
+    bo = ho.numel() * ho.element_size()
+
+    def run():
+        dq, dk, dv = (t.to(dev, non_blocking=True) for t in (hq, hk, hv))
+        o, _ = sa.sample_attention(dq, dk, dv, alpha=alpha, chunk_n=chunk_n, guard=args.guard, q_head0=q_head0,
+                                   group=group)
+        ho.copy_(o, non_blocking=True)
+
+    run()
+    torch.cuda.synchronize(dev)
+    ts = []
+    for _ in range(max(1, min(args.steps, 3))):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ts.append(e0.elapsed_time(e1))
+    t = sum(ts) / len(ts)
+    tt = torch.tensor([t], device=dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t = float(tt.item())
+    return {"value": round(dense_job / (t * 1e-3) / 1e12, 2), "unit": "TFLOP/s", "ms_per_step": round(t, 3),
+            "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo}
+
+
+def cpu_baseline(q, k, v, kv_heads, group, alpha, chunk_n, S, d):
+    """CPU oracle on head 0 (stage 1+2 full, stage 3 sampled), extrapolated."""
+    qh = q[0].double().cpu().numpy()
+    kh = k[kv_heads.index(0 // group)].double().cpu().numpy()
+    vh = v[kv_heads.index(0 // group)].double().cpu().numpy()
+    r = cpu_sample(qh, kh, vh, alpha, chunk_n)
+    val = dense_flops(S, d) / r["t_head"] / 1e12
+    return {"value": round(val, 5), "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
+            "sample": (f"head 0 of the same workload: stage 1+2 in full ({r['t_stage1'] + r['t_stage2']:.2f} s), "
+                       f"stage 3 on {r['sampled_qblocks']} seeded query blocks ({r['sampled_blocks']} of "
+                       f"{r['head_blocks']} kept blocks) extrapolated to the head ({r['t_stage3_extrapolated']:.1f} s); "
+                       f"per-head time {r['t_head']:.1f} s, every head costs the same"),
+            "density_head0": round(r["density"], 4)}
+
+
+def run_reference(args, rank, S, Hq, Hkv, d, alpha, chunk_n, workload):
+    """--impl reference: the reference's CPU algorithm (the pinned numpy port)
+    timed on this host, rank 0 only; every step is a bounded sample of the
+    workload (one head, stage 3 sampled) extrapolated per head."""
+    if rank != 0:
+        return
+    import torch
+
+    from paper_2406_15486_b200 import synth
+
+    q, k, v, kv = synth.make_inputs(S, Hq, Hkv, d, seed=args.seed, heads=[0], device="cpu")
+    qh, kh, vh = (t[0].double().numpy() for t in (q, k, v))
+    ts = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(qh, kh, vh, alpha, chunk_n, n_qblocks=4, seed=i)
+        if i >= args.warmup:
+            ts.append(r["t_head"])
+    t_head = sum(ts) / len(ts)
+    value = dense_flops(S, d) / t_head / 1e12
+    ms = t_head * Hq * 1e3
+    line = {"metric": "sparse prefill attention eff. TFLOP/s at 128K (ChatGLM3-6B shape, alpha=0.95)"
+            if args.config == "c3" else f"sparse prefill attention eff. TFLOP/s ({args.config})",
+            "value": round(value, 5), "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 1), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (same seeded generator, head 0)", "config": workload,
+            "impl": "reference",
+            "cpu_baseline": {"value": round(value, 5), "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
+                             "sample": "per step: head 0, stage 1+2 full, stage 3 on 4 seeded query blocks, "
+                                       "extrapolated to 32 heads"},
+            "e2e": {"value": round(value, 5), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -146,53 +146,78 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int i = quad * 32 + lane_id();  // query row within the block
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float sl2 = 1.4426950408889634f * 0.08838834764831845f;  // log2(e) / sqrt(128)
-    float m_ref = -INFINITY, l = 0.f;
+    const uint64_t sl2x2 = f32x2(sl2, sl2);
+    float m_ref = -INFINITY;
+    uint64_t lacc0 = f32x2(0.f, 0.f), lacc1 = f32x2(0.f, 0.f);  // packed row-sum partials
     for (int j = 0; j < n; ++j) {
       const int kb = __ldg(list + j);
-      const int lim = kb == qb ? i : 127;
+      const bool diag = kb == qb;  // warp-uniform: only the diagonal block needs the causal mask
       mbar_wait(&sm->s_full, j & 1);
       tc_fence_after();
-      float mx = -INFINITY;
+      // ---- pass 1: row max of the raw scores (FMNMX3, two chains)
+      float ma = -INFINITY, mb = -INFINITY;
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32];
-        tmem_ld32(tS + lane_off + ch * 32, r);
-        tmem_ld_wait();
+        tmem_ld32_sync(tS + lane_off + ch * 32, r);
+        if (diag) {
 #pragma unroll
-        for (int t = 0; t < 32; ++t)
-          if (ch * 32 + t <= lim) mx = fmaxf(mx, __uint_as_float(r[t]));
+          for (int t = 0; t < 32; ++t)
+            if (ch * 32 + t > i) r[t] = __float_as_uint(-INFINITY);
+        }
+#pragma unroll
+        for (int t = 0; t < 32; t += 4) {
+          ma = fmax3(ma, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
+          mb = fmax3(mb, __uint_as_float(r[t + 2]), __uint_as_float(r[t + 3]));
+        }
       }
-      const float mxs = mx * sl2;
+      const float mxs = fmaxf(ma, mb) * sl2;
       // tcgen05.ld/st are warp-collective: take the rescale decision per warp
       if (__any_sync(0xffffffffu, mxs > m_ref + kRescaleThreshold)) {
         const float m_new = fmaxf(m_ref, mxs);
         if (j > 0) {
           const float f = ex2(m_ref - m_new);
-          l *= f;
+          const uint64_t f2 = f32x2(f, f);
+          lacc0 = fmul2(lacc0, f2);
+          lacc1 = fmul2(lacc1, f2);
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             uint32_t r[32];
-            tmem_ld32(tO + lane_off + ch * 32, r);
-            tmem_ld_wait();
+            tmem_ld32_sync(tO + lane_off + ch * 32, r);
 #pragma unroll
-            for (int t = 0; t < 32; ++t) r[t] = __float_as_uint(__uint_as_float(r[t]) * f);
+            for (int t = 0; t < 32; t += 2) {
+              uint64_t v = fmul2(f32x2(__uint_as_float(r[t]), __uint_as_float(r[t + 1])), f2);
+              float a, b;
+              unpack_f32x2(v, a, b);
+              r[t] = __float_as_uint(a);
+              r[t + 1] = __float_as_uint(b);
+            }
             tmem_st32(tO + lane_off + ch * 32, r);
           }
         }
         m_ref = m_new;
       }
+      // ---- pass 2: P = exp2(s * log2e/sqrt(d) - m) -> bf16 into TMEM (aliasing S), row sum
+      const uint64_t negm = f32x2(-m_ref, -m_ref);
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32];
-        tmem_ld32(tS + lane_off + ch * 32, r);
-        tmem_ld_wait();
+        tmem_ld32_sync(tS + lane_off + ch * 32, r);
+        if (diag) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (ch * 32 + t > i) r[t] = __float_as_uint(-INFINITY);
+        }
         uint32_t pk[16];
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
-          const int c0 = ch * 32 + 2 * t;
-          const float p0 = c0 <= lim ? ex2(fmaf(__uint_as_float(r[2 * t]), sl2, -m_ref)) : 0.f;
-          const float p1 = c0 + 1 <= lim ? ex2(fmaf(__uint_as_float(r[2 * t + 1]), sl2, -m_ref)) : 0.f;
-          l += p0 + p1;
+          float y0, y1;
+          unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm), y0, y1);
+          const float p0 = ex2(y0), p1 = ex2(y1);
+          if (t & 1)
+            lacc1 = fadd2(lacc1, f32x2(p0, p1));
+          else
+            lacc0 = fadd2(lacc0, f32x2(p0, p1));
           pk[t] = pack_bf16(p0, p1);
         }
         tmem_st16(tS + lane_off + ch * 16, pk);
@@ -200,6 +225,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm->p_full);
+    }
+    float l;
+    {
+      float a0, a1, b0, b1;
+      unpack_f32x2(lacc0, a0, a1);
+      unpack_f32x2(lacc1, b0, b1);
+      l = (a0 + a1) + (b0 + b1);
     }
     // epilogue: O / l -> bf16
     mbar_wait(&sm->o_full, 0);
@@ -211,8 +243,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch) {
       uint32_t r[32];
-      tmem_ld32(tO + lane_off + ch * 32, r);
-      tmem_ld_wait();
+      tmem_ld32_sync(tO + lane_off + ch * 32, r);
       uint32_t pk[16];
 #pragma unroll
       for (int t = 0; t < 16; ++t)

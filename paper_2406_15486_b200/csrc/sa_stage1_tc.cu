@@ -206,14 +206,15 @@ __global__ void __launch_bounds__(kThreads, 2)
 __global__ void k1_rowfin(Stage1Geom g, const int* __restrict__ only, const float* __restrict__ pa,
                           const float* __restrict__ pb, const float* __restrict__ pm,
                           double* __restrict__ rowstat) {
-  const int hc = blockIdx.x;
+  const int hc = blockIdx.y;
   if (only && only[hc] == 0) return;
   const int c = hc % g.cn;
   const int se = g.S < 128 ? g.S : (c + 1) * g.itv;
   const int nr = g.S < 128 ? g.S : 128;
   const int nkb = (se + 127) / 128;
   const int lane = threadIdx.x & 31;
-  for (int rl = threadIdx.x >> 5; rl < nr; rl += blockDim.x >> 5) {
+  const int warps = blockDim.x >> 5;
+  for (int rl = blockIdx.x * warps + (threadIdx.x >> 5); rl < nr; rl += gridDim.x * warps) {
     const size_t o = ((size_t)hc * 128 + rl) * g.nb;
     float mx = -INFINITY;
     for (int kb = lane; kb < nkb; kb += 32) mx = fmaxf(mx, pm[o + kb]);
@@ -309,7 +310,7 @@ int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const in
   if (int e = check_launch("stage1 tcgen05")) return e;
   double* rowstat = reinterpret_cast<double*>(ws + L.rowstat);
   double* part3 = reinterpret_cast<double*>(ws + L.part3);
-  k1_rowfin<<<g.Hq * g.cn, 256, 0, st>>>(g, only, P.pa, P.pb, P.pm, rowstat);
+  k1_rowfin<<<dim3(16, g.Hq * g.cn), 256, 0, st>>>(g, only, P.pa, P.pb, P.pm, rowstat);
   if (int e = check_launch("stage1 rowfin")) return e;
   k1_fold<<<dim3(ceil_div(g.nb, 128), g.Hq * g.cn), 128, 0, st>>>(g, only, P.pa, P.pb, P.pm, rowstat,
                                                                   part3);

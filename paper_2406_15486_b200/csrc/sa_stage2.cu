@@ -253,15 +253,28 @@ __global__ void __launch_bounds__(1024) k2_sched(const int* __restrict__ kv_cnt,
   }
 }
 
-__global__ void k_check_finite_f32(const float* __restrict__ x, long long n, int* flag) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    if (!isfinite(x[i])) *flag = 1;
+// NaN/Inf scan, 16-byte vector loads (any non-finite element sets *flag).
+__device__ __forceinline__ bool bad_f32(uint32_t w) { return (w & 0x7f800000u) == 0x7f800000u; }
+__device__ __forceinline__ bool bad_bf16x2(uint32_t w) {
+  return (w & 0x7f80u) == 0x7f80u || (w & 0x7f800000u) == 0x7f800000u;
 }
-__global__ void k_check_finite_bf16(const unsigned short* __restrict__ x, long long n, int* flag) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    if ((x[i] & 0x7f80u) == 0x7f80u) *flag = 1;
+template <bool kBf16>
+__global__ void k_check_finite(const uint32_t* __restrict__ x, long long nwords,
+                               const unsigned short* __restrict__ tail16, int* flag) {
+  const uint4* x4 = reinterpret_cast<const uint4*>(x);
+  const long long n4 = nwords >> 2;
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const uint4 v = __ldg(x4 + i);
+    if (kBf16)
+      bad |= bad_bf16x2(v.x) | bad_bf16x2(v.y) | bad_bf16x2(v.z) | bad_bf16x2(v.w);
+    else
+      bad |= bad_f32(v.x) | bad_f32(v.y) | bad_f32(v.z) | bad_f32(v.w);
+  }
+  for (long long i = (n4 << 2) + blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += (long long)gridDim.x * blockDim.x)
+    bad |= kBf16 ? bad_bf16x2(x[i]) : bad_f32(x[i]);
+  if (tail16 && blockIdx.x == 0 && threadIdx.x == 0) bad |= (*tail16 & 0x7f80u) == 0x7f80u;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1;
 }
 
 }  // namespace
@@ -309,11 +322,17 @@ int launch_sched(const int* kv_cnt, int n_items, int nb, int* order, cudaStream_
 
 int launch_check_finite(const void* x, int dtype, long long n, int* flag, cudaStream_t st) {
   if (n <= 0) return SA_OK;
-  const int grid = (int)std::min<long long>(148LL * 8, (n + 255) / 256);
+  const int esize = dtype == SA_FP32 ? 4 : 2;
+  const long long bytes = n * esize;
+  const long long nwords = bytes / 4;
+  const int grid = (int)std::min<long long>(148LL * 16, std::max<long long>(1, (nwords / 4 + 255) / 256));
+  // odd bf16 count: the last element sits alone in a half word
+  const unsigned short* tail =
+      (dtype != SA_FP32 && (n & 1)) ? static_cast<const unsigned short*>(x) + (n - 1) : nullptr;
   if (dtype == SA_FP32)
-    k_check_finite_f32<<<grid, 256, 0, st>>>(static_cast<const float*>(x), n, flag);
+    k_check_finite<false><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(x), nwords, nullptr, flag);
   else
-    k_check_finite_bf16<<<grid, 256, 0, st>>>(static_cast<const unsigned short*>(x), n, flag);
+    k_check_finite<true><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(x), nwords, tail, flag);
   return check_launch("sa_check_finite");
 }
 
