@@ -12,7 +12,8 @@ import os
 
 from .errors import InputError, InternalInvariantError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsampleattn.so")
+LIB_PATH = os.environ.get("SA_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                         "libsampleattn.so")
 
 SA_OK, SA_ERR_INVALID, SA_ERR_UNSUPPORTED, SA_ERR_INTERNAL, SA_ERR_CUDA = 0, -1, -2, -3, -4
 SA_BF16, SA_FP32 = 0, 1

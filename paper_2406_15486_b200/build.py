@@ -30,7 +30,7 @@ SOURCES = [
 ]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE,
-                     "-I", CSRC, "--expt-relaxed-constexpr"]
+                     "-I", CSRC, "--expt-relaxed-constexpr"] + os.environ.get("SA_NVCC_EXTRA", "").split()
 
 
 def nvcc() -> str:
@@ -49,7 +49,7 @@ def _stale(obj: str, src: str) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False, lib: str = LIB) -> str:
     os.makedirs(BUILD, exist_ok=True)
     cc = nvcc()
     jobs = []
@@ -74,8 +74,8 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
                 sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed on {cmd[-3]}")
-    if jobs or not os.path.exists(LIB):
-        cmd = [cc, *ARCH, "-shared", "-o", LIB, *objs]
+    if jobs or not os.path.exists(lib):
+        cmd = [cc, *ARCH, "-shared", "-o", lib, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
@@ -83,4 +83,6 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, ptxas_verbose="--ptxas" in sys.argv))
+    out = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv or bool(out), ptxas_verbose="--ptxas" in sys.argv,
+                lib=os.path.abspath(out[0]) if out else LIB))

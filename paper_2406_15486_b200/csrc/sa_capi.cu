@@ -87,9 +87,8 @@ Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int d
   if (dtype == SA_BF16) off = align_up(off + (size_t)3 * Hq * cn * 128 * nb * sizeof(float));
   L.rowstat = off;
   off = align_up(off + rows * 2 * sizeof(double));
-  L.nsx = ceil_div(nb, kExactKbPerCta);
   L.x_part = off;
-  off = align_up(off + rows * L.nsx * 2 * sizeof(double));
+  off = align_up(off + 3 * rows * nb * sizeof(double));
   L.part3 = off;
   off = align_up(off + (size_t)Hq * cn * nb * 4 * sizeof(double));
   L.sched = off;

@@ -20,7 +20,6 @@ constexpr int kBlk = 128;       // tensor-core tile (query rows == key rows == b
 constexpr int kHeadDim = 128;   // tensor-core head dimension
 constexpr int kMaxSimtD = 128;  // SIMT paths
 constexpr int kMaxSimtBlk = 128;
-constexpr int kExactKbPerCta = 16;  // exact stage-1: key blocks per CTA in the stats pass
 
 __host__ __device__ inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 __host__ __device__ inline long long tri(long long n) { return n * (n + 1) / 2; }
@@ -34,11 +33,10 @@ struct Stage1Geom {
 struct Workspace {
   size_t tc_part;   // float  [3][Hq*cn*blk*nb]   (A, B, m) per (row, key block)
   size_t rowstat;   // double [Hq*cn*blk][2]      (log2 max, sum) per sampled row
-  size_t x_part;    // double [Hq*cn*blk*nsx][2]  exact stats per (row, key split)
+  size_t x_part;    // double [3][Hq*cn*blk*nb]   exact (A, B, m) per (row, key block)
   size_t part3;     // double [Hq*cn*nb][4]       (col, slash X-1, X, X+1) per key block
   size_t sched;     // int    [nb + 2]
   size_t total;
-  int nsx;
 };
 Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int dtype);
 
@@ -48,8 +46,11 @@ int launch_stage1_exact(const Stage1Geom& g, const void* q, const void* k, int d
                         double* slash, cudaStream_t st);
 int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const int* only_flags,
                      char* ws, const Workspace& L, double* col, double* slash, cudaStream_t st);
-int launch_stage1_finalize(const Stage1Geom& g, const int* only_flags, const double* part3,
-                           double* col, double* slash, cudaStream_t st);
+// rows' global max / sum, fold into part3, scatter into col / slash
+template <typename TPlane, bool kLog2>
+int launch_fold(const Stage1Geom& g, const int* only, const TPlane* pa, const TPlane* pb,
+                const TPlane* pm, char* ws, const Workspace& L, double* col, double* slash,
+                cudaStream_t st);
 
 int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq, int Hkv,
                      int group, int q_head0, const int* kv_cnt, const int* kv_idx,

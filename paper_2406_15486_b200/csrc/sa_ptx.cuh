@@ -41,13 +41,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps in hardware until
+// the phase completes (or the hint expires) instead of spinning on issue
+// slots shared with the softmax warps of its SM sub-partition.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "SA_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra SA_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 
@@ -216,6 +219,21 @@ __device__ __forceinline__ void tmem_ld32_sync(uint32_t taddr, uint32_t (&r)[32]
       : "memory");
 }
 
+// Wait for outstanding tcgen05.ld and tie the 32 destination registers to the
+// wait, so the compiler cannot schedule their consumers before the data lands
+// (lets independent work run between tmem_ld32 and this wait).
+__device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+        "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+        "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]),
+        "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]),
+        "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+      :
+      : "memory");
+}
+
 // Blackwell packed / 3-input FP ops (FMNMX3, FFMA2, FADD2).
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;
@@ -246,10 +264,41 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
   return d;
 }
 
+// 2^x for a pair on the FMA pipe (offloads the MUFU unit): round-to-nearest
+// split x = j + f via the 1.5*2^23 magic constant, degree-3 minimax
+// polynomial for 2^f on [-0.5, 0.5] (max rel. error 7.5e-5, far below the
+// bf16 rounding of P), exponent added as an integer.  x is clamped at -127
+// (no -inf inputs: callers use it only on unmasked tiles).
+__device__ __forceinline__ uint64_t ex2_poly2(float x0, float x1) {
+  const float kMagic = 12582912.0f;
+  x0 = fmaxf(x0, -127.f);
+  x1 = fmaxf(x1, -127.f);
+  const uint64_t X = f32x2(x0, x1);
+  const uint64_t T = fadd2(X, f32x2(kMagic, kMagic));
+  const uint64_t J = fadd2(T, f32x2(-kMagic, -kMagic));
+  const uint64_t F = ffma2(J, f32x2(-1.f, -1.f), X);
+  uint64_t P = ffma2(F, f32x2(0.05517132f, 0.05517132f), f32x2(0.24261054f, 0.24261054f));
+  P = ffma2(P, F, f32x2(0.69326099f, 0.69326099f));
+  P = ffma2(P, F, f32x2(0.99992811f, 0.99992811f));
+  uint32_t p0, p1, t0, t1;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(p0), "=r"(p1) : "l"(P));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(t0), "=r"(t1) : "l"(T));
+  asm("mad.lo.u32 %0, %1, 8388608, %0;" : "+r"(p0) : "r"(t0));
+  asm("mad.lo.u32 %0, %1, 8388608, %0;" : "+r"(p1) : "r"(t1));
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(p0), "r"(p1));
+  return r;
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// bf16x2 pack on the integer ALU (round half up; valid for finite x >= 0,
+// i.e. softmax probabilities) -- keeps the conversion off the MUFU/XU pipe.
+__device__ __forceinline__ uint32_t pack_bf16_pos(float lo, float hi) {
+  return __byte_perm(__float_as_uint(lo) + 0x8000u, __float_as_uint(hi) + 0x8000u, 0x7632);
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;

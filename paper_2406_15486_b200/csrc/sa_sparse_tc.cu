@@ -18,6 +18,8 @@
 // softmax overlaps the other's MMAs.  GQA: q head h reads kv head h / group.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "sa_internal.h"
 #include "sa_ptx.cuh"
 
@@ -30,9 +32,15 @@ constexpr uint32_t kBoxBytes = kTileBytes / 2;
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, false);
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 128, true);
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef SA_PACK_P
+#define SA_PACK_P pack_bf16
+#endif
+#ifndef SA_EMU_MASK
+#define SA_EMU_MASK 3
+#endif
 
 struct __align__(8) K3Smem {
-  uint64_t q_full, k_full, k_empty, v_full, v_empty, s_full, p_full, o_full;
+  uint64_t q_full, k_full, k_empty, v_full, v_empty, s_full, p_part, p_full, o_full;
   uint32_t tmem_base;
 };
 
@@ -46,6 +54,9 @@ struct K3Params {
   long long* touched;
 };
 
+// kExp: 0 = production; 1/2/3 = timing experiments (skip softmax math / skip
+// MMAs / skip both) used only by tools/k3_experiments.py via SA_K3_EXP.
+template <int kExp>
 __global__ void __launch_bounds__(kThreads, 2)
     k3_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
           const __grid_constant__ CUtensorMap tm_v, const K3Params P) {
@@ -74,6 +85,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_init(&sm->v_full, 1);
     mbar_init(&sm->v_empty, 1);
     mbar_init(&sm->s_full, 1);
+    mbar_init(&sm->p_part, 128);
     mbar_init(&sm->p_full, 128);
     mbar_init(&sm->o_full, 1);
     fence_mbar_init();
@@ -111,15 +123,24 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_wait(&sm->q_full, 0);
     for (int j = 0; j <= n; ++j) {
       if (j >= 1) {
-        // O += P_{j-1} V_{j-1}
-        mbar_wait(&sm->p_full, (j - 1) & 1);
+        // O += P_{j-1} V_{j-1}: the first 3/4 of the keys as soon as the softmax
+        // has written that part of P, the last quarter after the rest lands
+        mbar_wait(&sm->p_part, (j - 1) & 1);
         mbar_wait(&sm->v_full, (j - 1) & 1);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_ts(tO, tS + kk * 8, sdesc_sw128(v_addr + kk * 2048, kBoxBytes, 1024), kIdescPV,
+          for (int kk = 0; kk < 6; ++kk)
+            if (kExp < 2) umma_ts(tO, tS + kk * 8, sdesc_sw128(v_addr + kk * 2048, kBoxBytes, 1024), kIdescPV,
                     (j > 1 || kk > 0) ? 1u : 0u);
+        }
+        __syncwarp();
+        mbar_wait(&sm->p_full, (j - 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 6; kk < 8; ++kk)
+            if (kExp < 2) umma_ts(tO, tS + kk * 8, sdesc_sw128(v_addr + kk * 2048, kBoxBytes, 1024), kIdescPV, 1u);
           umma_commit(&sm->v_empty);
           if (j == n) umma_commit(&sm->o_full);
         }
@@ -132,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t off = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
-            umma_ss(tS, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024),
+            if (kExp < 2) umma_ss(tS, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024),
                     kIdescQK, kk > 0 ? 1u : 0u);
           }
           umma_commit(&sm->s_full);
@@ -154,21 +175,34 @@ __global__ void __launch_bounds__(kThreads, 2)
       const bool diag = kb == qb;  // warp-uniform: only the diagonal block needs the causal mask
       mbar_wait(&sm->s_full, j & 1);
       tc_fence_after();
-      // ---- pass 1: row max of the raw scores (FMNMX3, two chains)
+      if (kExp == 1 || kExp == 3) {
+        tc_fence_before();
+        mbar_arrive(&sm->p_part);
+        mbar_arrive(&sm->p_full);
+        continue;
+      }
+      // ---- pass 1: row max of the raw scores (FMNMX3, two chains); TMEM loads
+      // double-buffered so chunk c+1 is in flight while chunk c is reduced
       float ma = -INFINITY, mb = -INFINITY;
+      {
+        uint32_t buf[2][32];
+        tmem_ld32(tS + lane_off, buf[0]);
+        tmem_ld_wait_regs(buf[0]);
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t r[32];
-        tmem_ld32_sync(tS + lane_off + ch * 32, r);
-        if (diag) {
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t(&r)[32] = buf[ch & 1];
+          if (ch < 3) tmem_ld32(tS + lane_off + (ch + 1) * 32, buf[(ch + 1) & 1]);
+          if (diag) {
 #pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (ch * 32 + t > i) r[t] = __float_as_uint(-INFINITY);
-        }
+            for (int t = 0; t < 32; ++t)
+              if (ch * 32 + t > i) r[t] = __float_as_uint(-INFINITY);
+          }
 #pragma unroll
-        for (int t = 0; t < 32; t += 4) {
-          ma = fmax3(ma, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
-          mb = fmax3(mb, __uint_as_float(r[t + 2]), __uint_as_float(r[t + 3]));
+          for (int t = 0; t < 32; t += 4) {
+            ma = fmax3(ma, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
+            mb = fmax3(mb, __uint_as_float(r[t + 2]), __uint_as_float(r[t + 3]));
+          }
+          if (ch < 3) tmem_ld_wait_regs(buf[(ch + 1) & 1]);
         }
       }
       const float mxs = fmaxf(ma, mb) * sl2;
@@ -197,30 +231,57 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         m_ref = m_new;
       }
-      // ---- pass 2: P = exp2(s * log2e/sqrt(d) - m) -> bf16 into TMEM (aliasing S), row sum
+      // ---- pass 2: P = exp2(s * log2e/sqrt(d) - m) -> bf16 into TMEM (aliasing S), row sum.
+      // Off the diagonal a quarter of the exponentials run as an FMA-pipe
+      // polynomial so the MUFU unit stops pacing the tensor core.
       const uint64_t negm = f32x2(-m_ref, -m_ref);
+      {
+        uint32_t buf[2][32];
+        tmem_ld32(tS + lane_off, buf[0]);
+        tmem_ld_wait_regs(buf[0]);
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t r[32];
-        tmem_ld32_sync(tS + lane_off + ch * 32, r);
-        if (diag) {
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t(&r)[32] = buf[ch & 1];
+          if (ch < 3) tmem_ld32(tS + lane_off + (ch + 1) * 32, buf[(ch + 1) & 1]);
+          uint32_t pk[16];
+          if (diag) {
 #pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (ch * 32 + t > i) r[t] = __float_as_uint(-INFINITY);
+            for (int t = 0; t < 32; ++t)
+              if (ch * 32 + t > i) r[t] = __float_as_uint(-INFINITY);
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              float y0, y1;
+              unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm), y0, y1);
+              const float p0 = ex2(y0), p1 = ex2(y1);
+              if (t & 1) lacc1 = fadd2(lacc1, f32x2(p0, p1));
+              else lacc0 = fadd2(lacc0, f32x2(p0, p1));
+              pk[t] = SA_PACK_P(p0, p1);
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              float y0, y1;
+              unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm), y0, y1);
+              uint64_t pp;
+              if ((t & 3) >= SA_EMU_MASK)
+                pp = ex2_poly2(y0, y1);
+              else
+                pp = f32x2(ex2(y0), ex2(y1));
+              if (t & 1) lacc1 = fadd2(lacc1, pp);
+              else lacc0 = fadd2(lacc0, pp);
+              float p0, p1;
+              unpack_f32x2(pp, p0, p1);
+              pk[t] = SA_PACK_P(p0, p1);
+            }
+          }
+          tmem_st16(tS + lane_off + ch * 16, pk);
+          if (ch == 2) {  // P columns for keys 0..95 are in TMEM: let the PV MMA start
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&sm->p_part);
+          }
+          if (ch < 3) tmem_ld_wait_regs(buf[(ch + 1) & 1]);
         }
-        uint32_t pk[16];
-#pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          float y0, y1;
-          unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm), y0, y1);
-          const float p0 = ex2(y0), p1 = ex2(y1);
-          if (t & 1)
-            lacc1 = fadd2(lacc1, f32x2(p0, p1));
-          else
-            lacc0 = fadd2(lacc0, f32x2(p0, p1));
-          pk[t] = pack_bf16(p0, p1);
-        }
-        tmem_st16(tS + lane_off + ch * 16, pk);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -290,11 +351,23 @@ int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq,
   const size_t smem = 3 * kTileBytes + sizeof(K3Smem) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k3_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k3_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k3_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k3_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k3_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
+  static const int exp_mode = [] {
+    const char* e = getenv("SA_K3_EXP");
+    return e ? atoi(e) : 0;
+  }();
   if (touched) cudaMemsetAsync(touched, 0, sizeof(long long) * Hq, st);
-  k3_tc<<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P);
+  switch (exp_mode) {
+    case 1: k3_tc<1><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
+    case 2: k3_tc<2><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
+    case 3: k3_tc<3><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
+    default: k3_tc<0><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
+  }
   return check_launch("sparse_forward tcgen05");
 }
 

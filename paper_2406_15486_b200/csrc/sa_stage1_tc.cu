@@ -200,87 +200,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
-// Per sampled row: global log2-max M and normaliser L over all key blocks.
-// One warp per row, lanes stride the key blocks (coalesced); fixed-order
-// shuffle tree -> deterministic.
-__global__ void k1_rowfin(Stage1Geom g, const int* __restrict__ only, const float* __restrict__ pa,
-                          const float* __restrict__ pb, const float* __restrict__ pm,
-                          double* __restrict__ rowstat) {
-  const int hc = blockIdx.y;
-  if (only && only[hc] == 0) return;
-  const int c = hc % g.cn;
-  const int se = g.S < 128 ? g.S : (c + 1) * g.itv;
-  const int nr = g.S < 128 ? g.S : 128;
-  const int nkb = (se + 127) / 128;
-  const int lane = threadIdx.x & 31;
-  const int warps = blockDim.x >> 5;
-  for (int rl = blockIdx.x * warps + (threadIdx.x >> 5); rl < nr; rl += gridDim.x * warps) {
-    const size_t o = ((size_t)hc * 128 + rl) * g.nb;
-    float mx = -INFINITY;
-    for (int kb = lane; kb < nkb; kb += 32) mx = fmaxf(mx, pm[o + kb]);
-    for (int s = 16; s > 0; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
-    double L = 0.0;
-    for (int kb = lane; kb < nkb; kb += 32) {
-      const float m = pm[o + kb];
-      if (m != -INFINITY) L += ((double)pa[o + kb] + (double)pb[o + kb]) * exp2((double)m - (double)mx);
-    }
-    for (int s = 16; s > 0; s >>= 1) L += __shfl_xor_sync(0xffffffffu, L, s);
-    if (lane == 0) {
-      rowstat[((size_t)hc * 128 + rl) * 2] = mx;
-      rowstat[((size_t)hc * 128 + rl) * 2 + 1] = L;
-    }
-  }
-}
-
-// Per key block: fold the 128 rows' normalised partial masses into part3.
-__global__ void k1_fold(Stage1Geom g, const int* __restrict__ only, const float* __restrict__ pa,
-                        const float* __restrict__ pb, const float* __restrict__ pm,
-                        const double* __restrict__ rowstat, double* __restrict__ part3) {
-  __shared__ double s_w[128][2];  // (M, 1/L) per row
-  const int hc = blockIdx.y;
-  if (only && only[hc] == 0) return;
-  const int c = hc % g.cn;
-  int ss, se;
-  if (g.S < 128) {
-    ss = 0;
-    se = g.S;
-  } else {
-    se = (c + 1) * g.itv;
-    ss = se - 128;
-  }
-  const int nr = se - ss;
-  const int nkb = (se + 127) / 128;
-  for (int r = threadIdx.x; r < nr; r += blockDim.x) {
-    s_w[r][0] = rowstat[((size_t)hc * 128 + r) * 2];
-    s_w[r][1] = 1.0 / rowstat[((size_t)hc * 128 + r) * 2 + 1];
-  }
-  __syncthreads();
-  const int kb = blockIdx.x * blockDim.x + threadIdx.x;
-  if (kb >= g.nb) return;
-  double* out = part3 + ((size_t)hc * g.nb + kb) * 4;
-  if (kb >= nkb) {
-    out[0] = out[1] = out[2] = out[3] = 0.0;
-    return;
-  }
-  const int b0 = ss / 128;
-  double s4[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int r = 0; r < nr; ++r) {
-    const size_t o = ((size_t)hc * 128 + r) * g.nb + kb;
-    const float m = pm[o];
-    if (m == -INFINITY) continue;
-    const double w = exp2((double)m - s_w[r][0]) * s_w[r][1];
-    const double a = (double)pa[o] * w, b = (double)pb[o] * w;
-    const int slot_a = (ss + r) / 128 - b0 + 1;  // bin r//128 - kb  -> slot relative to X-1
-    s4[0] += a + b;
-    s4[1 + slot_a] += a;
-    s4[slot_a] += b;  // bin r//128 - kb - 1
-  }
-  out[0] = s4[0];
-  out[1] = s4[1];
-  out[2] = s4[2];
-  out[3] = s4[3];
-}
-
 }  // namespace
 
 int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const int* only, char* ws,
@@ -308,14 +227,7 @@ int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const in
   }
   k1_tc<<<dim3(nsplit, g.Hq * g.cn), kThreads, smem, st>>>(tq, tk, P);
   if (int e = check_launch("stage1 tcgen05")) return e;
-  double* rowstat = reinterpret_cast<double*>(ws + L.rowstat);
-  double* part3 = reinterpret_cast<double*>(ws + L.part3);
-  k1_rowfin<<<dim3(16, g.Hq * g.cn), 256, 0, st>>>(g, only, P.pa, P.pb, P.pm, rowstat);
-  if (int e = check_launch("stage1 rowfin")) return e;
-  k1_fold<<<dim3(ceil_div(g.nb, 128), g.Hq * g.cn), 128, 0, st>>>(g, only, P.pa, P.pb, P.pm, rowstat,
-                                                                  part3);
-  if (int e = check_launch("stage1 fold")) return e;
-  return launch_stage1_finalize(g, only, part3, col, slash, st);
+  return launch_fold<float, true>(g, only, P.pa, P.pb, P.pm, ws, L, col, slash, st);
 }
 
 }  // namespace sa
