@@ -41,6 +41,7 @@ CONFIGS = {
     "c3": (131072, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 128K, bf16, alpha 0.95, chunk_n 1"),
     "c2": (32768, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 32K, bf16, alpha 0.95, chunk_n 1"),
     "c4": (98304, 32, 8, 0.95, 15, "InternLM2-7B attention shape, seq 96K, bf16, alpha 0.95, 2% sampling"),
+    "c5": (1048576, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 1M, bf16, alpha 0.95, heads sharded + NVLink gather"),
 }
 
 
@@ -53,47 +54,69 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms by ONE
+    background nvidia-smi process, started before the timed region (so no
+    fork/exec happens while kernels are being timed); only samples whose
+    timestamps fall inside the marked window are summarised."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
-        self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
+        self.proc = None
+        self.t0 = self.t1 = None
 
-    def _run(self):
-        while not self._stop.is_set():
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def stop(self):
+        rows = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                out, _ = self.proc.communicate(timeout=10)
             except Exception:
-                pass
-            self._stop.wait(0.2)
+                out = ""
+            import datetime
 
-    def __enter__(self):
-        self._t.start()
-        return self
-
-    def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+            for line in out.splitlines():
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 7:
+                    continue
+                try:
+                    ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    continue
+                rows.append((ts, f[1:]))
+        self.all_rows = [r for _, r in rows]
+        win = [r for ts, r in rows if self.t0 is not None and self.t0 - 0.15 <= ts <= (self.t1 or ts) + 0.15]
+        self.rows = win or self.all_rows[-3:]
 
     def summary(self):
-        if not self.rows:
+        rows = getattr(self, "rows", [])
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
 
 
 def dense_flops(S: int, d: int, blk: int = 128) -> int:
@@ -178,6 +201,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--guard", default="auto", choices=["auto", "always", "never"])
+    ap.add_argument("--chunk-n", type=int, default=None)
+    ap.add_argument("--gather", action="store_true", help="all-gather outputs over NCCL (default for c5)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -187,9 +212,13 @@ def main():
     S, Hq, Hkv, alpha, chunk_n, desc = CONFIGS[args.config]
     if args.alpha is not None:
         alpha = args.alpha
+    if args.chunk_n is not None:
+        chunk_n = args.chunk_n
+    gather = args.gather or args.config == "c5"
     d = 128
     workload = {"workload": desc, "S": S, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d, "alpha": alpha,
-                "chunk_n": chunk_n, "blk": 128, "parallelism": f"heads/{world}", "l2": "flushed between steps"}
+                "chunk_n": chunk_n, "blk": 128, "parallelism": f"heads/{world}" + ("+gather" if gather else ""),
+                "l2": "flushed between steps"}
 
     if args.impl == "reference":
         return run_reference(args, rank, S, Hq, Hkv, d, alpha, chunk_n, workload)
@@ -213,8 +242,33 @@ def main():
     q_head0 = my_heads[0]
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     out = torch.empty_like(q)
+    from paper_2406_15486_b200.parallel import sample_attention_sharded, shard_heads
+
+    shard = shard_heads(Hq, Hkv, world, rank)
+
+    class _Res:  # stage timings are not split per chunk in the gathered path
+        def __init__(self, masks):
+            self.masks = masks
+            self.mask = masks[-1]
+
+        def stage_ms(self):
+            return {"stage1_ms": 0.0, "stage2_ms": 0.0, "stage3_ms": 0.0}
+
+        def n_rescored(self):
+            return 0
 
     def step(timings=False):
+        if gather and world > 1:
+            masks = []
+
+            def fn(qq, kk, vv, **kw2):
+                o_, r_ = sa.sample_attention(qq, kk, vv, **kw2)
+                masks.append(r_.mask)
+                return o_, r_
+
+            sample_attention_sharded(q, k, v, shard, heads_per_chunk=1, compute_fn=fn, alpha=alpha,
+                                     chunk_n=chunk_n, guard=args.guard)
+            return out, _Res(masks)
         return sa.sample_attention(q, k, v, alpha=alpha, chunk_n=chunk_n, guard=args.guard, timings=timings,
                                    q_head0=q_head0, group=group, out=out)
 
@@ -229,9 +283,12 @@ def main():
 
     # ---- timed region (device-resident inputs)
     step_ms, k3_ms, s1_ms, s2_ms = [], [], [], []
+    clk = ClockSampler(local_rank)
+    clk.start()
     launches0 = _lib.launch_count()
     barrier()
-    with ClockSampler(local_rank) as clk:
+    clk.mark_start()
+    if True:
         for _ in range(args.steps):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -245,7 +302,9 @@ def main():
             s1_ms.append(st["stage1_ms"])
             s2_ms.append(st["stage2_ms"])
     barrier()
+    clk.mark_end()
     launches = _lib.launch_count() - launches0
+    clk.stop()
     t_step = sum(step_ms) / len(step_ms)
     t_local = torch.tensor([t_step], device=dev)
     if world > 1:
@@ -253,12 +312,16 @@ def main():
     t_max = float(t_local.item())
 
     # ---- work accounting (after timing; host syncs allowed)
-    mask = res.mask
-    flop = sa.flop_accounting(mask, S, d)
-    kept = flop.estimated_flops_sparse
+    masks = getattr(res, "masks", [res.mask])
+    flops = [sa.flop_accounting(m, S, d) for m in masks]
+    kept = sum(f.estimated_flops_sparse for f in flops)
+    flop = flops[0]
+    flop.block_density = sum(f.active_blocks for f in flops) / sum(f.causal_blocks for f in flops)
     dense_job = dense_flops(S, d) * Hq
     value = dense_job / (t_max * 1e-3) / 1e12
     t_k3 = sum(k3_ms) / len(k3_ms)
+    if t_k3 <= 0:  # gathered path: kernel time not separated, charge the whole step
+        t_k3 = t_step
     pk, pk_kind = peaks()
     achieved = kept / (t_k3 * 1e-3) / 1e12
     traffic = None

@@ -111,10 +111,10 @@ int sa_merge(const int* k_sel, const int* idx_sel, int Hq, int chunk_n, int nb, 
 /* Full causal block mask (every kb <= qb): the dense-attention comparison row. */
 int sa_full_mask(int Hq, int nb, int* kv_cnt, int* kv_idx, void* stream);
 
-/* Longest-first work order over (head, query block) items from kv_cnt:
- * order[i] = h*nb + qb, sorted by descending block count. */
-int sa_schedule(const int* kv_cnt, int Hq, int nb, int* order, void* workspace,
-                size_t workspace_bytes, void* stream);
+/* Work order over (head, query block) items from kv_cnt: order[i] = h*nb + qb,
+ * grouped by KV head (GQA group, so one KV head's K/V stays L2-resident while
+ * its items run) and longest-first (descending block count) inside a group. */
+int sa_schedule(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* order, void* stream);
 
 /* Stage 3 — replaces sparse_attention (executor.py:104-158): per (head,
  * query block) the online-softmax recurrence over the mask's ascending key

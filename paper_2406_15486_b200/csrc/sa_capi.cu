@@ -24,7 +24,7 @@ int launch_merge(const int* k_sel, const int* idx_sel, int Hq, int cn, int nb, i
                  int itv, int sink_blocks, int local_blocks, int* kv_cnt, int* kv_idx,
                  long long* ab, long long* ae, cudaStream_t st);
 int launch_full(int Hq, int nb, int* kv_cnt, int* kv_idx, cudaStream_t st);
-int launch_sched(const int* kv_cnt, int n_items, int nb, int* order, cudaStream_t st);
+int launch_sched(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* order, cudaStream_t st);
 int launch_check_finite(const void* x, int dtype, long long n, int* flag, cudaStream_t st);
 
 namespace {
@@ -194,12 +194,10 @@ int sa_full_mask(int Hq, int nb, int* kv_cnt, int* kv_idx, void* stream) {
   return launch_full(Hq, nb, kv_cnt, kv_idx, static_cast<cudaStream_t>(stream));
 }
 
-int sa_schedule(const int* kv_cnt, int Hq, int nb, int* order, void* workspace,
-                size_t workspace_bytes, void* stream) {
-  (void)workspace;
-  (void)workspace_bytes;
+int sa_schedule(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* order, void* stream) {
   if (Hq < 1 || nb < 1 || !kv_cnt || !order) return fail(SA_ERR_INVALID, "sa_schedule: bad args");
-  return launch_sched(kv_cnt, Hq * nb, nb, order, static_cast<cudaStream_t>(stream));
+  if (group < 1 || q_head0 < 0) return fail(SA_ERR_INVALID, "sa_schedule: bad group / q_head0");
+  return launch_sched(kv_cnt, Hq, nb, group, q_head0, order, static_cast<cudaStream_t>(stream));
 }
 
 int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, int S, int Hq, int Hkv,

@@ -226,19 +226,29 @@ __global__ void k2_full(int Hq, int nb, int* __restrict__ kv_cnt, int* __restric
   if (threadIdx.x == 0) kv_cnt[item] = qb + 1;
 }
 
-// counting sort of work items by descending block count (single CTA)
-__global__ void __launch_bounds__(1024) k2_sched(const int* __restrict__ kv_cnt, int n_items, int nb,
-                                                 int* __restrict__ order) {
+// Counting sort of work items by descending block count, one CTA per KV
+// group: the q heads of a group are contiguous, so its items are the
+// contiguous range [seg_lo, seg_hi) of h*nb + qb, and sorting each group's
+// range in place yields a group-major, longest-first order.  Group-major keeps
+// one KV head's K/V (64 MiB at 128K) resident in L2 while its items run.
+__global__ void __launch_bounds__(1024) k2_sched(const int* __restrict__ kv_cnt, int Hq, int nb, int group,
+                                                 int q_head0, int* __restrict__ order) {
   extern __shared__ int hist[];  // [nb + 2]
+  // heads of local kv group blockIdx.x
+  const int g_first = q_head0 / group;
+  int h_lo = max(0, (g_first + (int)blockIdx.x) * group - q_head0);
+  int h_hi = min(Hq, (g_first + (int)blockIdx.x + 1) * group - q_head0);
+  if (h_lo >= h_hi) return;
+  const int lo = h_lo * nb, hi = h_hi * nb;
   for (int i = threadIdx.x; i < nb + 2; i += blockDim.x) hist[i] = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < n_items; i += blockDim.x) {
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     int c = min(max(kv_cnt[i], 0), nb);
     atomicAdd(hist + c, 1);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int run = 0;  // descending: bin nb first
+    int run = lo;  // descending: bin nb first
     for (int c = nb; c >= 0; --c) {
       const int v = hist[c];
       hist[c] = run;
@@ -246,7 +256,7 @@ __global__ void __launch_bounds__(1024) k2_sched(const int* __restrict__ kv_cnt,
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < n_items; i += blockDim.x) {
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     int c = min(max(kv_cnt[i], 0), nb);
     const int slot = atomicAdd(hist + c, 1);
     order[slot] = i;
@@ -312,11 +322,12 @@ int launch_full(int Hq, int nb, int* kv_cnt, int* kv_idx, cudaStream_t st) {
   return check_launch("sa_full_mask");
 }
 
-int launch_sched(const int* kv_cnt, int n_items, int nb, int* order, cudaStream_t st) {
+int launch_sched(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* order, cudaStream_t st) {
   const size_t smem = (size_t)(nb + 2) * 4;
   if (smem > 200 * 1024) return fail(SA_ERR_UNSUPPORTED, "sa_schedule: nb too large");
   cudaFuncSetAttribute(k2_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k2_sched<<<1, 1024, smem, st>>>(kv_cnt, n_items, nb, order);
+  const int n_groups = (q_head0 + Hq - 1) / group - q_head0 / group + 1;
+  k2_sched<<<n_groups, 1024, smem, st>>>(kv_cnt, Hq, nb, group, q_head0, order);
   return check_launch("sa_schedule");
 }
 

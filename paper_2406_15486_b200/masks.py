@@ -251,12 +251,14 @@ class BlockMask:
         return cls(blk, S, cnt, idx)
 
     # ------------------------------------------------------------ scheduling
-    def order(self) -> torch.Tensor:
-        """Longest-first (head, query block) work order (sa_schedule), cached."""
-        if self._order is None:
+    def order(self, group: int = 1, q_head0: int = 0) -> torch.Tensor:
+        """KV-group-major, longest-first (head, query block) work order
+        (sa_schedule), cached per (group, q_head0)."""
+        key = (group, q_head0)
+        if self._order is None or self._order[0] != key:
             nb = self.n_qblocks
             order = torch.empty(self.n_heads * nb, dtype=torch.int32, device=self.device)
-            _lib.call("sa_schedule", self.kv_cnt.data_ptr(), self.n_heads, nb, order.data_ptr(), None, 0,
+            _lib.call("sa_schedule", self.kv_cnt.data_ptr(), self.n_heads, nb, group, q_head0, order.data_ptr(),
                       torch.cuda.current_stream(self.device).cuda_stream)
-            self._order = order
-        return self._order
+            self._order = (key, order)
+        return self._order[1]

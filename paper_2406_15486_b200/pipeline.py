@@ -78,7 +78,7 @@ def sample_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, alpha: f
         ev[1].record()
     sel = select(reduced, cfg, guard=guard)
     mask = merge_index(sel, plan, cfg.blk, batch.S, sink_blocks, local_blocks)
-    mask.order()
+    mask.order(batch.group, batch.q_head0)
     if ev:
         ev[2].record()
     lse = torch.empty((batch.Hq, batch.S), dtype=torch.float32, device=batch.q.device) if return_lse else None

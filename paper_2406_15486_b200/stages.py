@@ -348,7 +348,7 @@ def sparse_attention(heads, mask: BlockMask, out: torch.Tensor | None = None,
     touched = torch.zeros(b.Hq, dtype=torch.int64, device=b.q.device) if report else None
     _lib.call("sa_sparse_forward", b.q.data_ptr(), b.k.data_ptr(), b.v.data_ptr(), b.dtype_code, b.S, b.Hq,
               b.Hkv, b.d, mask.blk, b.group, b.q_head0, mask.kv_cnt.data_ptr(), mask.kv_idx.data_ptr(),
-              mask.order().data_ptr(), out.data_ptr(), None if lse is None else lse.data_ptr(),
+              mask.order(b.group, b.q_head0).data_ptr(), out.data_ptr(), None if lse is None else lse.data_ptr(),
               None if touched is None else touched.data_ptr(), b.stream)
     if not report:
         return out, None
