@@ -26,6 +26,7 @@ SOURCES = [
     "sa_stage1_tc.cu",
     "sa_stage2.cu",
     "sa_sparse_tc.cu",
+    "sa_sparse_tc2.cu",
     "sa_sparse_simt.cu",
 ]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

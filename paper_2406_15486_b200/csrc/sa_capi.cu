@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <mutex>
 #include <string>
@@ -207,9 +208,17 @@ int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, in
   if (!q || !k || !v || !kv_cnt || !kv_idx || !out)
     return fail(SA_ERR_INVALID, "sa_sparse_forward: null pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (dtype == SA_BF16)
-    return launch_sparse_tc(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse,
-                            touched, st);
+  if (dtype == SA_BF16) {
+    static const int impl = [] {
+      const char* e = getenv("SA_K3_IMPL");
+      return (e && e[0] == 's') ? 1 : 0;  // "single": one tile per CTA, two CTAs per SM
+    }();
+    if (impl == 1)
+      return launch_sparse_tc(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse,
+                              touched, st);
+    return launch_sparse_tc_pair(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse,
+                                 touched, st);
+  }
   return launch_sparse_simt(static_cast<const float*>(q), static_cast<const float*>(k),
                             static_cast<const float*>(v), S, Hq, Hkv, d, blk, group, q_head0, kv_cnt,
                             kv_idx, order, static_cast<float*>(out), lse, touched, st);

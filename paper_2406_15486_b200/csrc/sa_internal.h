@@ -56,6 +56,10 @@ int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq,
                      int group, int q_head0, const int* kv_cnt, const int* kv_idx,
                      const int* order, void* out, float* lse, long long* touched,
                      cudaStream_t st);
+int launch_sparse_tc_pair(const void* q, const void* k, const void* v, int S, int Hq, int Hkv,
+                          int group, int q_head0, const int* kv_cnt, const int* kv_idx,
+                          const int* order, void* out, float* lse, long long* touched,
+                          cudaStream_t st);
 int launch_sparse_simt(const float* q, const float* k, const float* v, int S, int Hq, int Hkv,
                        int d, int blk, int group, int q_head0, const int* kv_cnt,
                        const int* kv_idx, const int* order, float* out, float* lse,

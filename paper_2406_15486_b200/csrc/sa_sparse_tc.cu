@@ -39,6 +39,20 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define SA_EMU_MASK 3
 #endif
 
+#ifndef SA_K3_PROF
+#define SA_K3_PROF 0
+#endif
+// Optional cycle accounting (build with -DSA_K3_PROF=1; read via
+// sa_debug_k3_profile): where the softmax / MMA / TMA roles spend time.
+__device__ unsigned long long g_k3_prof[16];
+#if SA_K3_PROF
+#define PROF_T0() const long long _pt0 = clock64()
+#define PROF_ADD(slot) prof[slot] += clock64() - _pt0
+#else
+#define PROF_T0()
+#define PROF_ADD(slot)
+#endif
+
 struct __align__(8) K3Smem {
   uint64_t q_full, k_full, k_empty, v_full, v_empty, s_full, p_part, p_full, o_full;
   uint32_t tmem_base;
@@ -74,6 +88,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int* list = P.kv_idx + (size_t)h * tri(P.nb) + tri(qb);
   const int kvh = kv_head_of(h, P.group, P.q_head0);
   const int warp = warp_id();
+#if SA_K3_PROF
+  long long prof[16] = {0};
+  const long long t_start = clock64();
+#endif
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tm_q);
@@ -108,11 +126,19 @@ __global__ void __launch_bounds__(kThreads, 2)
       tma_load_3d(sQ + kBoxBytes, &tm_q, &sm->q_full, 64, qb * 128, h);
       for (int j = 0; j < n; ++j) {
         const int key0 = __ldg(list + j) * 128;
-        if (j >= 1) mbar_wait(&sm->k_empty, (j - 1) & 1);
+        if (j >= 1) {
+          PROF_T0();
+          mbar_wait(&sm->k_empty, (j - 1) & 1);
+          PROF_ADD(9);
+        }
         mbar_expect_tx(&sm->k_full, kTileBytes);
         tma_load_3d_hint(sK, &tm_k, &sm->k_full, 0, key0, kvh, keep);
         tma_load_3d_hint(sK + kBoxBytes, &tm_k, &sm->k_full, 64, key0, kvh, keep);
-        if (j >= 1) mbar_wait(&sm->v_empty, (j - 1) & 1);
+        if (j >= 1) {
+          PROF_T0();
+          mbar_wait(&sm->v_empty, (j - 1) & 1);
+          PROF_ADD(10);
+        }
         mbar_expect_tx(&sm->v_full, kTileBytes);
         tma_load_3d_hint(sV, &tm_v, &sm->v_full, 0, key0, kvh, keep);
         tma_load_3d_hint(sV + kBoxBytes, &tm_v, &sm->v_full, 64, key0, kvh, keep);
@@ -125,8 +151,16 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (j >= 1) {
         // O += P_{j-1} V_{j-1}: the first 3/4 of the keys as soon as the softmax
         // has written that part of P, the last quarter after the rest lands
-        mbar_wait(&sm->p_part, (j - 1) & 1);
-        mbar_wait(&sm->v_full, (j - 1) & 1);
+        {
+          PROF_T0();
+          mbar_wait(&sm->p_part, (j - 1) & 1);
+          PROF_ADD(5);
+        }
+        {
+          PROF_T0();
+          mbar_wait(&sm->v_full, (j - 1) & 1);
+          PROF_ADD(6);
+        }
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -135,7 +169,11 @@ __global__ void __launch_bounds__(kThreads, 2)
                     (j > 1 || kk > 0) ? 1u : 0u);
         }
         __syncwarp();
-        mbar_wait(&sm->p_full, (j - 1) & 1);
+        {
+          PROF_T0();
+          mbar_wait(&sm->p_full, (j - 1) & 1);
+          PROF_ADD(7);
+        }
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -147,7 +185,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncwarp();
       }
       if (j < n) {
-        mbar_wait(&sm->k_full, j & 1);
+        {
+          PROF_T0();
+          mbar_wait(&sm->k_full, j & 1);
+          PROF_ADD(8);
+        }
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -173,7 +215,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int j = 0; j < n; ++j) {
       const int kb = __ldg(list + j);
       const bool diag = kb == qb;  // warp-uniform: only the diagonal block needs the causal mask
-      mbar_wait(&sm->s_full, j & 1);
+      {
+        PROF_T0();
+        mbar_wait(&sm->s_full, j & 1);
+        PROF_ADD(0);
+      }
+#if SA_K3_PROF
+      long long _p1 = clock64();
+#endif
       tc_fence_after();
       if (kExp == 1 || kExp == 3) {
         tc_fence_before();
@@ -183,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       // ---- pass 1: row max of the raw scores (FMNMX3, two chains); TMEM loads
       // double-buffered so chunk c+1 is in flight while chunk c is reduced
-      float ma = -INFINITY, mb = -INFINITY;
+      float ma = -INFINITY, mb = -INFINITY, mc = -INFINITY, md = -INFINITY;
       {
         uint32_t buf[2][32];
         tmem_ld32(tS + lane_off, buf[0]);
@@ -198,14 +247,20 @@ __global__ void __launch_bounds__(kThreads, 2)
               if (ch * 32 + t > i) r[t] = __float_as_uint(-INFINITY);
           }
 #pragma unroll
-          for (int t = 0; t < 32; t += 4) {
+          for (int t = 0; t < 32; t += 8) {  // four independent FMNMX3 chains
             ma = fmax3(ma, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
             mb = fmax3(mb, __uint_as_float(r[t + 2]), __uint_as_float(r[t + 3]));
+            mc = fmax3(mc, __uint_as_float(r[t + 4]), __uint_as_float(r[t + 5]));
+            md = fmax3(md, __uint_as_float(r[t + 6]), __uint_as_float(r[t + 7]));
           }
           if (ch < 3) tmem_ld_wait_regs(buf[(ch + 1) & 1]);
         }
       }
-      const float mxs = fmaxf(ma, mb) * sl2;
+#if SA_K3_PROF
+      prof[1] += clock64() - _p1;
+      _p1 = clock64();
+#endif
+      const float mxs = fmax3(fmaxf(ma, mb), mc, md) * sl2;
       // tcgen05.ld/st are warp-collective: take the rescale decision per warp
       if (__any_sync(0xffffffffu, mxs > m_ref + kRescaleThreshold)) {
         const float m_new = fmaxf(m_ref, mxs);
@@ -231,6 +286,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         m_ref = m_new;
       }
+#if SA_K3_PROF
+      prof[2] += clock64() - _p1;
+      _p1 = clock64();
+#endif
       // ---- pass 2: P = exp2(s * log2e/sqrt(d) - m) -> bf16 into TMEM (aliasing S), row sum.
       // Off the diagonal a quarter of the exponentials run as an FMA-pipe
       // polynomial so the MUFU unit stops pacing the tensor core.
@@ -263,7 +322,9 @@ __global__ void __launch_bounds__(kThreads, 2)
               float y0, y1;
               unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm), y0, y1);
               uint64_t pp;
-              if ((t & 3) >= SA_EMU_MASK)
+              if (kExp == 4)
+                pp = f32x2(y0, y1);  // timing experiment: no exponentials at all
+              else if ((t & 3) >= SA_EMU_MASK)
                 pp = ex2_poly2(y0, y1);
               else
                 pp = f32x2(ex2(y0), ex2(y1));
@@ -286,6 +347,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm->p_full);
+#if SA_K3_PROF
+      prof[3] += clock64() - _p1;
+#endif
     }
     float l;
     {
@@ -295,7 +359,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       l = (a0 + a1) + (b0 + b1);
     }
     // epilogue: O / l -> bf16
-    mbar_wait(&sm->o_full, 0);
+    {
+      PROF_T0();
+      mbar_wait(&sm->o_full, 0);
+      PROF_ADD(4);
+    }
     tc_fence_after();
     const int row = qb * 128 + i;
     const bool valid = row < P.S;
@@ -319,6 +387,20 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (threadIdx.x == 64 && P.touched)
       atomicAdd(reinterpret_cast<unsigned long long*>(P.touched + h), (unsigned long long)n);
   }
+#if SA_K3_PROF
+  if (lane_id() == 0 && warp != 0) {  // softmax warps (slots 0-4), MMA warp (5-8)
+    for (int k = 0; k < 9; ++k)
+      if (prof[k]) atomicAdd(&g_k3_prof[k], (unsigned long long)prof[k]);
+    if (warp == 1) {
+      atomicAdd(&g_k3_prof[11], (unsigned long long)(clock64() - t_start));
+      atomicAdd(&g_k3_prof[12], (unsigned long long)n);
+    }
+  }
+  if (warp == 0 && lane_id() == 0) {
+    atomicAdd(&g_k3_prof[9], (unsigned long long)prof[9]);
+    atomicAdd(&g_k3_prof[10], (unsigned long long)prof[10]);
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -355,6 +437,7 @@ int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq,
     cudaFuncSetAttribute(k3_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k3_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k3_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k3_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   static const int exp_mode = [] {
@@ -366,9 +449,19 @@ int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq,
     case 1: k3_tc<1><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
     case 2: k3_tc<2><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
     case 3: k3_tc<3><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
+    case 4: k3_tc<4><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
     default: k3_tc<0><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
   }
   return check_launch("sparse_forward tcgen05");
 }
 
 }  // namespace sa
+
+extern "C" int sa_debug_k3_profile(unsigned long long* out16, int reset) {
+  cudaMemcpyFromSymbol(out16, sa::g_k3_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(sa::g_k3_prof, z, sizeof(z));
+  }
+  return 0;
+}

@@ -20,8 +20,9 @@ fl = 4 * 128 * sum(128 * (qb * 128 + 128) for qb in range(S // 128)) * H
 print(json.dumps({"ms": min(ts), "tflops": fl / min(ts) / 1e9}))
 '''
 libs = sys.argv[1:] or [""]
+modes = [int(m) for m in os.environ.get("MODES", "0,1,2,3").split(",")]
 for lib in libs:
-    for mode in (0, 1, 2, 3):
+    for mode in modes:
         env = dict(os.environ, SA_K3_EXP=str(mode))
         if lib:
             env["SA_LIB_PATH"] = os.path.abspath(lib)
