@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from .errors import InputError
 
-__all__ = ["AttentionHead", "HeadSet", "HeadBatch", "check_finite"]
+__all__ = ["AttentionHead", "HeadSet", "HeadBatch", "check_finite", "check_finite_async"]
 
 _DTYPES = {torch.bfloat16: _lib.SA_BF16, torch.float32: _lib.SA_FP32}
 
@@ -89,6 +89,13 @@ class HeadSet:
 
 def _stream(t: torch.Tensor) -> int:
     return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def check_finite_async(tensors, flag: torch.Tensor, stream: int) -> None:
+    """Queue the NaN/Inf scan of `tensors` on `stream`, OR-ing into the int32
+    device flag; the caller reads the flag later (no synchronisation here)."""
+    for t in tensors:
+        _lib.call("sa_check_finite", t.data_ptr(), _DTYPES[t.dtype], t.numel(), flag.data_ptr(), stream)
 
 
 def check_finite(*tensors: torch.Tensor) -> None:

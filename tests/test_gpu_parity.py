@@ -217,3 +217,45 @@ def test_determinism(sa):
     assert torch.equal(o1, o2)
     assert r1.mask.serialize() if r1.mask.n_heads == 1 else True
     assert torch.equal(r1.mask.kv_cnt, r2.mask.kv_cnt)
+
+
+@pytest.mark.parametrize("growth", [0.0, 40.0, 400.0])
+def test_sparse_kernel_extreme_and_growing_logits(sa, growth):
+    """Logits that grow by `growth` nats along the key axis force the stage-3
+    softmax to move its reference max mid-tile (the overflow rebase path);
+    the outputs must stay finite and match the oracle (ref
+    tests/test_executor.py:101-108 checks extreme logits stay finite)."""
+    rng = np.random.default_rng(7)
+    S = 1024
+    q = np.ones((S, 128)) * 0.25 + 0.01 * rng.standard_normal((S, 128))
+    k = 0.01 * rng.standard_normal((S, 128))
+    k[:, 0] += np.linspace(0.0, growth, S) * np.sqrt(128) / (0.25 * 1)  # logit_j ~ growth * j / S
+    v = rng.standard_normal((S, 128))
+    q, k, v = (O_bf16(a) for a in (q, k, v))
+    nb = S // 128
+    grid = np.tril(np.ones((nb, nb), dtype=bool))
+    mask = sa.BlockMask.from_dense(128, grid, S=S)
+    qt, kt, vt = to_dev((q, k, v), torch.bfloat16)
+    out, _ = sa.sparse_attention(sa.HeadBatch.from_tensors(qt, kt, vt), mask)
+    got = out[0].float().cpu().numpy()
+    assert np.isfinite(got).all()
+    ref, _ = O.sparse_attention(q, k, v, grid, 128)
+    assert np.abs(got - ref).max() <= BF16_TOL
+
+
+def test_host_streaming_matches_device_path(sa):
+    """sample_attention_host (pinned host buffers, overlapped copies) gives the
+    same output and selections as sample_attention on device tensors."""
+    from paper_2406_15486_b200 import synth
+    q, k, v, _ = synth.make_inputs(2048, 8, 2, seed=3, device="cuda")
+    o_dev, r_dev = sa.sample_attention(q, k, v, alpha=0.95, chunk_n=2)
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    o_host, res = sa.sample_attention_host(hq, hk, hv, alpha=0.95, chunk_n=2, heads_per_group=2)
+    assert torch.equal(o_host, o_dev.cpu())
+    sel_dev = r_dev.mask.selections()
+    sel_host = [s for r in res for s in r.mask.selections()]
+    assert [[(c.i_c, c.i_s) for c in s.chunks] for s in sel_dev] == [[(c.i_c, c.i_s) for c in s.chunks] for s in sel_host]
+    bad = hq.clone()
+    bad[3, 5, 7] = float("inf")
+    with pytest.raises(sa.InputError):
+        sa.sample_attention_host(bad, hk, hv, alpha=0.95, chunk_n=2)
