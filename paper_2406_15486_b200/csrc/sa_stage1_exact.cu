@@ -65,20 +65,15 @@ __device__ void stage(double* dst, const T* src, int n, int d, int c0) {
   }
 }
 
+// Work of one CTA: key blocks [kb0, kb1) of (head, chunk) hc.
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 1)
-    xf_pass(const T* __restrict__ q, const T* __restrict__ k, Stage1Geom g, const int* __restrict__ only,
-            int kb_per_cta, double* __restrict__ pa, double* __restrict__ pb, double* __restrict__ pm) {
-  extern __shared__ double smem_d[];
-  double* qs = smem_d;                          // [kRows][kDChunk+1]
-  double* ks = smem_d + kRows * (kDChunk + 1);  // [kKeys][kDChunk+1]
-  const int hc = blockIdx.y;
-  if (only && only[hc] == 0) return;
+__device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __restrict__ k, const Stage1Geom& g,
+                                        int hc, int kb0, int kb1, double* __restrict__ pa,
+                                        double* __restrict__ pb, double* __restrict__ pm, double* qs,
+                                        double* ks) {
   const int h = hc / g.cn, c = hc - h * g.cn;
   const Win w = window_of(c, g.S, g.blk, g.itv);
-  const int kb0 = blockIdx.x * kb_per_cta;
-  if (kb0 >= w.nkb) return;
-  const int kb1 = min(w.nkb, kb0 + kb_per_cta);
+  kb1 = min(kb1, w.nkb);
   const int kvh = kv_head_of(h, g.group, g.q_head0);
   const int nr = w.se - w.ss, d = g.d, blk = g.blk;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -156,6 +151,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+}
+
+
+// One CTA per (head, chunk, key-block split).  For the guard's re-score
+// (`only` flags) every key block gets its own CTA so the few flagged pairs
+// spread over all SMs; CTAs of unflagged pairs exit at once.
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    xf_pass(const T* __restrict__ q, const T* __restrict__ k, Stage1Geom g, const int* __restrict__ only,
+            int kb_per_cta, double* __restrict__ pa, double* __restrict__ pb, double* __restrict__ pm) {
+  extern __shared__ double smem_d[];
+  double* qs = smem_d;                          // [kRows][kDChunk+1]
+  double* ks = smem_d + kRows * (kDChunk + 1);  // [kKeys][kDChunk+1]
+  const int hc = blockIdx.y;
+  if (only && only[hc] == 0) return;
+  const int kb0 = blockIdx.x * kb_per_cta;
+  xf_work(q, k, g, hc, kb0, kb0 + kb_per_cta, pa, pb, pm, qs, ks);
 }
 
 }  // namespace
@@ -289,8 +301,6 @@ int run_exact(const Stage1Geom& g, const T* q, const T* k, const int* only, char
   double* pb = pa + plane;
   double* pm = pb + plane;
   const long long work = (long long)g.Hq * g.cn * g.nb;
-  // a guard re-score touches a handful of pairs: split them finely so they
-  // spread over the SMs (unflagged pairs' CTAs exit at once)
   const int kpc = only ? 1 : (int)std::max<long long>(2, std::min<long long>(32, work / (148LL * 4)));
   xf_pass<T><<<dim3(ceil_div(g.nb, kpc), g.Hq * g.cn), kThreads, smem, st>>>(q, k, g, only, kpc, pa, pb, pm);
   if (int e = check_launch("stage1 exact pass")) return e;
