@@ -65,13 +65,16 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
+        self.interval_ms = int(os.environ.get("SA_CLOCK_MS", "100"))
         self.proc = None
         self.t0 = self.t1 = None
 
     def start(self):
+        if self.interval_ms <= 0:
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None

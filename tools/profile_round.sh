@@ -13,6 +13,6 @@ timeout 300 python bench.py --config c2 --no-cpu > $OUT/bench_c2.json 2>> $OUT/b
 timeout 600 python bench.py --config c4 --no-cpu --no-e2e > $OUT/bench_c4.json 2>> $OUT/bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   timeout 300 python bench.py --steps 2 --warmup 3 --no-dense --no-cpu --no-e2e > $OUT/ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k3_tc|k1_tc|k2_select|k2_merge|xf_pass|s1_fold" -s 0 -c 12 \
+ncu --set full --clock-control none --import-source on -k regex:"k3_pair|k3_tc|k1_tc|k2_select|k2_merge|xf_pass|s1_fold" -s 0 -c 12 \
   -o $OUT/full timeout 600 python bench.py --steps 1 --warmup 3 --no-dense --no-cpu --no-e2e > $OUT/ncu_full.log 2>&1
 ls -la $OUT
