@@ -205,6 +205,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--guard", default="auto", choices=["auto", "always", "never"])
     ap.add_argument("--chunk-n", type=int, default=None)
+    ap.add_argument("--no-graph", action="store_true", help="launch the stages from Python instead of CUDA graphs")
     ap.add_argument("--gather", action="store_true", help="all-gather outputs over NCCL (default for c5)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -260,7 +261,32 @@ def main():
         def n_rescored(self):
             return 0
 
+    use_graph = not (gather and world > 1) and not args.no_graph
+    gexec = None
+    if use_graph:  # the serving path: the three stages captured as CUDA graphs on static buffers
+        gexec = sa.SampleAttentionGraph(q, k, v, alpha=alpha, chunk_n=chunk_n, guard=args.guard, group=group,
+                                        q_head0=q_head0)
+
+    class _GraphRes:
+        def __init__(self, ev):
+            self.mask, self.masks, self.ev = gexec.mask, [gexec.mask], ev
+
+        def stage_ms(self):
+            e = self.ev
+            return {"stage1_ms": e[0].elapsed_time(e[1]), "stage2_ms": e[1].elapsed_time(e[2]),
+                    "stage3_ms": e[2].elapsed_time(e[3])}
+
+        def n_rescored(self):
+            return gexec.n_rescored()
+
     def step(timings=False):
+        if gexec is not None:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record()
+            for i in range(3):
+                gexec.replay_stage(i)
+                ev[i + 1].record()
+            return gexec.out, _GraphRes(ev)
         if gather and world > 1:
             masks = []
 
@@ -306,8 +332,11 @@ def main():
             s2_ms.append(st["stage2_ms"])
     barrier()
     clk.mark_end()
-    launches = _lib.launch_count() - launches0
+    # graph replays do not pass through the C ABI: count the captured kernels per replay
+    launches = gexec.kernels_per_replay * args.steps if gexec is not None else _lib.launch_count() - launches0
     clk.stop()
+    if gexec is not None:
+        gexec.check()
     t_step = sum(step_ms) / len(step_ms)
     t_local = torch.tensor([t_step], device=dev)
     if world > 1:
@@ -370,7 +399,8 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (seeded GPU generator: Zipf column sinks + local band + slash band + noise)",
                 "config": workload, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk.summary(), **extra}
+                "gpu_launches": launches, "clocks": clk.summary(),
+                "launch_path": "CUDA graphs (SampleAttentionGraph)" if gexec is not None else "eager", **extra}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

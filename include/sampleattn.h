@@ -111,9 +111,15 @@ int sa_merge(const int* k_sel, const int* idx_sel, int Hq, int chunk_n, int nb, 
 /* Full causal block mask (every kb <= qb): the dense-attention comparison row. */
 int sa_full_mask(int Hq, int nb, int* kv_cnt, int* kv_idx, void* stream);
 
-/* Work order over (head, query block) items from kv_cnt: order[i] = h*nb + qb,
- * grouped by KV head (GQA group, so one KV head's K/V stays L2-resident while
- * its items run) and longest-first (descending block count) inside a group. */
+/* Stage-3 work units.  A unit is two (head, query block) items that read the
+ * same KV head (two q heads of one GQA group at the same query block, or
+ * adjacent query blocks of a group's odd head out), run by one CTA that loads
+ * each K/V tile of the union of their block lists once.  sa_schedule writes
+ * order[2*u], order[2*u+1] = h*nb + qb of unit u's items (-1: no partner),
+ * grouped by KV head (one KV head's K/V stays L2-resident while its units run)
+ * and longest-first (descending kv_cnt[a] + kv_cnt[b]) inside a group.
+ * sa_schedule_len returns the entry count 2 * n_units (or < 0 on bad args). */
+int sa_schedule_len(int Hq, int nb, int group, int q_head0);
 int sa_schedule(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* order, void* stream);
 
 /* Stage 3 — replaces sparse_attention (executor.py:104-158): per (head,
@@ -121,7 +127,8 @@ int sa_schedule(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* 
  * blocks, entry-level causality inside the diagonal block.  out is
  * [Hq][S][d] in the input dtype; lse [Hq][S] fp32 (natural log) and
  * touched[Hq] (blocks processed, FlopReport.active_blocks) are optional.
- * order may be NULL (natural order). */
+ * order is sa_schedule's unit list (sa_schedule_len entries) or NULL
+ * (natural unit order). */
 int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, int S, int Hq,
                       int Hkv, int d, int blk, int group, int q_head0, const int* kv_cnt,
                       const int* kv_idx, const int* order, void* out, float* lse,

@@ -17,6 +17,7 @@ from .heads import AttentionHead, HeadBatch, HeadSet, check_finite
 from .masks import BlockMask, ChunkSelection, SelectedIndices
 from .pipeline import (ORACLE_CAP, HeadMetrics, MetricsReport, SampleAttentionResult, dense_attention,
                        run_pipeline, sample_attention)
+from .graph import SampleAttentionGraph
 from .streaming import sample_attention_host
 from .stages import (GUARD_EPS, ChunkScores, FlopReport, ReducedScores, SampledScores, arg_topk, block_reduce,
                      find_k, flop_accounting, merge_index, sample_scores, select, select_and_merge,
@@ -27,7 +28,7 @@ __version__ = "0.1.0"
 __all__ = [
     "AttentionHead", "BlockMask", "ChunkPlan", "ChunkScores", "ChunkSelection", "FlopReport",
     "GUARD_EPS", "GeneratorError", "HeadBatch", "HeadMetrics", "HeadSet", "InfeasibleGridError", "InputError",
-    "InternalInvariantError", "MetricsReport", "ORACLE_CAP", "ReducedScores", "SampleAttentionResult",
+    "InternalInvariantError", "MetricsReport", "SampleAttentionGraph", "ORACLE_CAP", "ReducedScores", "SampleAttentionResult",
     "SampledRange", "SampledScores", "SelectedIndices", "SparseConfig", "arg_topk", "block_reduce",
     "check_finite", "dense_attention", "find_k", "flop_accounting", "merge_index", "n_blocks", "plan_chunks",
     "resolve_config", "run_pipeline", "sample_attention", "sample_attention_host", "sample_scores", "select", "select_and_merge",

@@ -17,7 +17,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-BUILD = os.path.join(ROOT, "build", "obj")
+_EXTRA = os.environ.get("SA_NVCC_EXTRA", "").split()
+# experiment builds (extra -D flags) keep their objects apart from the product build
+BUILD = os.path.join(ROOT, "build", "obj" + ("_" + "_".join(f.strip("-").replace("=", "") for f in _EXTRA) if _EXTRA else ""))
 LIB = os.path.join(PKG, "libsampleattn.so")
 
 SOURCES = [
@@ -26,12 +28,12 @@ SOURCES = [
     "sa_stage1_tc.cu",
     "sa_stage2.cu",
     "sa_sparse_tc.cu",
-    "sa_sparse_tc2.cu",
+    "sa_sparse_share.cu",
     "sa_sparse_simt.cu",
 ]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE,
-                     "-I", CSRC, "--expt-relaxed-constexpr"] + os.environ.get("SA_NVCC_EXTRA", "").split()
+                     "-I", CSRC, "--expt-relaxed-constexpr"] + _EXTRA
 
 
 def nvcc() -> str:

@@ -201,6 +201,11 @@ int sa_schedule(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* 
   return launch_sched(kv_cnt, Hq, nb, group, q_head0, order, static_cast<cudaStream_t>(stream));
 }
 
+int sa_schedule_len(int Hq, int nb, int group, int q_head0) {
+  if (Hq < 1 || nb < 1 || group < 1 || q_head0 < 0) return fail(SA_ERR_INVALID, "sa_schedule_len: bad args");
+  return 2 * n_units(Hq, nb, group, q_head0);
+}
+
 int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, int S, int Hq, int Hkv,
                       int d, int blk, int group, int q_head0, const int* kv_cnt, const int* kv_idx,
                       const int* order, void* out, float* lse, long long* touched, void* stream) {
@@ -208,20 +213,21 @@ int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, in
   if (!q || !k || !v || !kv_cnt || !kv_idx || !out)
     return fail(SA_ERR_INVALID, "sa_sparse_forward: null pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int n_order = order ? 2 * n_units(Hq, ceil_div(S, blk), group, q_head0) : 0;
   if (dtype == SA_BF16) {
     static const int impl = [] {
       const char* e = getenv("SA_K3_IMPL");
-      return (e && e[0] == 's') ? 1 : 0;  // "single": one tile per CTA, two CTAs per SM
+      return (e && e[0] == 's') ? 1 : 0;  // "single": one item per CTA, two CTAs per SM (no K/V sharing)
     }();
     if (impl == 1)
-      return launch_sparse_tc(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse,
+      return launch_sparse_tc(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, n_order, out, lse,
                               touched, st);
-    return launch_sparse_tc_pair(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse,
-                                 touched, st);
+    return launch_sparse_share(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse, touched,
+                               st);
   }
   return launch_sparse_simt(static_cast<const float*>(q), static_cast<const float*>(k),
                             static_cast<const float*>(v), S, Hq, Hkv, d, blk, group, q_head0, kv_cnt,
-                            kv_idx, order, static_cast<float*>(out), lse, touched, st);
+                            kv_idx, order, n_order, static_cast<float*>(out), lse, touched, st);
 }
 
 }  // extern "C"

@@ -54,15 +54,11 @@ int launch_fold(const Stage1Geom& g, const int* only, const TPlane* pa, const TP
 
 int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq, int Hkv,
                      int group, int q_head0, const int* kv_cnt, const int* kv_idx,
-                     const int* order, void* out, float* lse, long long* touched,
+                     const int* order, int n_order, void* out, float* lse, long long* touched,
                      cudaStream_t st);
-int launch_sparse_tc_pair(const void* q, const void* k, const void* v, int S, int Hq, int Hkv,
-                          int group, int q_head0, const int* kv_cnt, const int* kv_idx,
-                          const int* order, void* out, float* lse, long long* touched,
-                          cudaStream_t st);
 int launch_sparse_simt(const float* q, const float* k, const float* v, int S, int Hq, int Hkv,
                        int d, int blk, int group, int q_head0, const int* kv_cnt,
-                       const int* kv_idx, const int* order, float* out, float* lse,
+                       const int* kv_idx, const int* order, int n_order, float* out, float* lse,
                        long long* touched, cudaStream_t st);
 
 // TMA descriptor for a contiguous [H][S][d] bf16 tensor, box {64, 128, 1}, 128B swizzle.
@@ -71,5 +67,49 @@ bool make_tmap_bf16_hsd(CUtensorMap* map, const void* base, int H, int S, int d)
 __host__ __device__ inline int kv_head_of(int h, int group, int q_head0) {
   return (q_head0 + h) / group - q_head0 / group;
 }
+
+// ---- stage-3 work units: two (head, query block) items that read the same
+// KV head, so one CTA loads each listed K/V tile once for both.  The local q
+// heads of a KV group pair up (h_lo, h_lo+1), (h_lo+2, h_lo+3), ... at the same
+// query block; an odd head out pairs adjacent query blocks (2j, 2j+1).
+// Items are h * nb + qb; a missing partner is -1.
+__host__ __device__ inline int n_local_kv(int Hq, int group, int q_head0) {
+  return kv_head_of(Hq - 1, group, q_head0) + 1;
+}
+__host__ __device__ inline void kv_group_heads(int g, int Hq, int group, int q_head0, int& lo, int& hi) {
+  const int g_first = q_head0 / group;
+  lo = (g_first + g) * group - q_head0;
+  hi = lo + group;
+  if (lo < 0) lo = 0;
+  if (hi > Hq) hi = Hq;
+}
+__host__ __device__ inline int units_of_group(int nh, int nb) {
+  return (nh / 2) * nb + ((nh & 1) ? (nb + 1) / 2 : 0);
+}
+__host__ __device__ inline void unit_items(int u, int h_lo, int nh, int nb, int& a, int& b) {
+  const int paired = (nh / 2) * nb;
+  if (u < paired) {
+    const int p = u / nb, qb = u - p * nb;
+    a = (h_lo + 2 * p) * nb + qb;
+    b = a + nb;
+  } else {
+    const int qb = 2 * (u - paired);
+    a = (h_lo + nh - 1) * nb + qb;
+    b = qb + 1 < nb ? a + 1 : -1;
+  }
+}
+__host__ __device__ inline int n_units(int Hq, int nb, int group, int q_head0) {
+  int total = 0;
+  for (int g = 0, G = n_local_kv(Hq, group, q_head0); g < G; ++g) {
+    int lo, hi;
+    kv_group_heads(g, Hq, group, q_head0, lo, hi);
+    total += units_of_group(hi - lo, nb);
+  }
+  return total;
+}
+
+int launch_sparse_share(const void* q, const void* k, const void* v, int S, int Hq, int Hkv, int group,
+                        int q_head0, const int* kv_cnt, const int* kv_idx, const int* units, void* out,
+                        float* lse, long long* touched, cudaStream_t st);
 
 }  // namespace sa

@@ -1,0 +1,210 @@
+// Stage-3 softmax warpgroup of one 128-row query tile (shared by the
+// tensor-core stage-3 kernels).  ref executor.py:124-151: per listed key block
+// s = (q/sqrt(d)) k^T, -inf above the diagonal only on the diagonal block,
+// online max / sum, O = sum P V, out = O / l.
+//
+// One query row per thread (= TMEM lane).  S (fp32, 128 TMEM columns) is read
+// twice, row max then exponentials, with the TMEM loads double-buffered; bf16 P
+// is written over S (columns [0, 64)) for the A-from-TMEM PV MMA.  The first
+// 3/4 of P is published early (p_part) so the PV MMA starts before the last
+// quarter lands.  Off the diagonal a quarter of the exponentials run as an
+// FMA-pipe polynomial so the MUFU pipe does not pace the tensor core.  O is
+// rescaled in TMEM only when the running max grows by more than 2^8.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "sa_internal.h"
+#include "sa_ptx.cuh"
+
+namespace sa {
+
+struct K3Tile {
+  int n, h, qb, kvh;
+  const int* list;  // ascending key blocks of (h, qb)
+};
+
+struct K3TileBars {
+  uint64_t* s_full;  // S(j) landed in TMEM           (tcgen05.commit)
+  uint64_t* p_part;  // P(j) keys 0..95 in TMEM        (128 arrivals)
+  uint64_t* p_full;  // P(j) complete                  (128 arrivals)
+  uint64_t* o_full;  // last PV done                   (tcgen05.commit)
+};
+
+constexpr float kK3RescaleThreshold = 8.0f;  // log2 units
+
+// Fraction of off-diagonal exponentials computed by the FMA-pipe polynomial:
+// SA_K3_POLY n -> n/4 (build-time experiment knob; production 1).
+#ifndef SA_K3_POLY
+#define SA_K3_POLY 1
+#endif
+// SA_K3_EXP (timing experiments only): 1 = no softmax math (arrive at once),
+// 2 = no exponentials (P = the scaled score, finite garbage).
+#ifndef SA_K3_EXP
+#define SA_K3_EXP 0
+#endif
+
+
+__device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBars& b, uint32_t tS0,
+                                                uint32_t tO0, int quad, int S, __nv_bfloat16* out,
+                                                float* lse, long long* touched) {
+  const int i = quad * 32 + lane_id();  // query row within the tile
+  const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+  const uint32_t tS = tS0 + lane_off, tO = tO0 + lane_off;
+  const float sl2 = 1.4426950408889634f * 0.08838834764831845f;  // log2(e) / sqrt(128)
+  const uint64_t sl2x2 = f32x2(sl2, sl2);
+  float m_ref = -INFINITY;
+  uint64_t lacc0 = f32x2(0.f, 0.f), lacc1 = f32x2(0.f, 0.f);
+  for (int j = 0; j < T.n; ++j) {
+    const int kb = __ldg(T.list + j);
+    const bool diag = kb == T.qb;  // warp-uniform
+    k3_wait(b.s_full, j & 1);
+    tc_fence_after();
+    if (SA_K3_EXP == 1) {
+      tc_fence_before();
+      mbar_arrive(b.p_part);
+      mbar_arrive(b.p_full);
+      continue;
+    }
+    // ---- pass 1: row max (four FMNMX3 chains)
+    float ma = -INFINITY, mb = -INFINITY, mc = -INFINITY, md = -INFINITY;
+    {
+      uint32_t buf[2][32];
+      tmem_ld32(tS, buf[0]);
+      tmem_ld_wait_regs(buf[0]);
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t(&r)[32] = buf[ch & 1];
+        if (ch < 3) tmem_ld32(tS + (ch + 1) * 32, buf[(ch + 1) & 1]);
+        if (diag) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (ch * 32 + t > i) r[t] = __float_as_uint(-INFINITY);
+        }
+#pragma unroll
+        for (int t = 0; t < 32; t += 8) {
+          ma = fmax3(ma, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
+          mb = fmax3(mb, __uint_as_float(r[t + 2]), __uint_as_float(r[t + 3]));
+          mc = fmax3(mc, __uint_as_float(r[t + 4]), __uint_as_float(r[t + 5]));
+          md = fmax3(md, __uint_as_float(r[t + 6]), __uint_as_float(r[t + 7]));
+        }
+        if (ch < 3) tmem_ld_wait_regs(buf[(ch + 1) & 1]);
+      }
+    }
+    const float mxs = fmax3(fmaxf(ma, mb), mc, md) * sl2;
+    // tcgen05.ld/st are warp-collective: rescale decision per warp.  O is
+    // stable here: PV(j-1) completed before S(j) did (in-order tensor pipe).
+    if (__any_sync(0xffffffffu, mxs > m_ref + kK3RescaleThreshold)) {
+      const float m_new = fmaxf(m_ref, mxs);
+      if (j > 0) {
+        const float f = ex2(m_ref - m_new);
+        const uint64_t f2 = f32x2(f, f);
+        lacc0 = fmul2(lacc0, f2);
+        lacc1 = fmul2(lacc1, f2);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t r[32];
+          tmem_ld32_sync(tO + ch * 32, r);
+#pragma unroll
+          for (int t = 0; t < 32; t += 2) {
+            uint64_t v = fmul2(f32x2(__uint_as_float(r[t]), __uint_as_float(r[t + 1])), f2);
+            float a, c;
+            unpack_f32x2(v, a, c);
+            r[t] = __float_as_uint(a);
+            r[t + 1] = __float_as_uint(c);
+          }
+          tmem_st32(tO + ch * 32, r);
+        }
+      }
+      m_ref = m_new;
+    }
+    // ---- pass 2: P = exp2(s*log2e/sqrt(d) - m) -> bf16 over S, row sum
+    const uint64_t negm = f32x2(-m_ref, -m_ref);
+    {
+      uint32_t buf[2][32];
+      tmem_ld32(tS, buf[0]);
+      tmem_ld_wait_regs(buf[0]);
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t(&r)[32] = buf[ch & 1];
+        if (ch < 3) tmem_ld32(tS + (ch + 1) * 32, buf[(ch + 1) & 1]);
+        uint32_t pk[16];
+        if (diag) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (ch * 32 + t > i) r[t] = __float_as_uint(-INFINITY);
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            float y0, y1;
+            unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm),
+                         y0, y1);
+            const float p0 = ex2(y0), p1 = ex2(y1);
+            if (t & 1)
+              lacc1 = fadd2(lacc1, f32x2(p0, p1));
+            else
+              lacc0 = fadd2(lacc0, f32x2(p0, p1));
+            pk[t] = pack_bf16(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            float y0, y1;
+            unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm),
+                         y0, y1);
+            const uint64_t pp = SA_K3_EXP == 2 ? f32x2(y0, y1)
+                                : ((t & 3) >= 4 - SA_K3_POLY) ? ex2_poly2(y0, y1)
+                                                              : f32x2(ex2(y0), ex2(y1));
+            if (t & 1)
+              lacc1 = fadd2(lacc1, pp);
+            else
+              lacc0 = fadd2(lacc0, pp);
+            float p0, p1;
+            unpack_f32x2(pp, p0, p1);
+            pk[t] = pack_bf16(p0, p1);
+          }
+        }
+        tmem_st16(tS + ch * 16, pk);
+        if (ch == 2) {  // keys 0..95 of P are in TMEM: let the PV MMA start
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(b.p_part);
+        }
+        if (ch < 3) tmem_ld_wait_regs(buf[(ch + 1) & 1]);
+      }
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    mbar_arrive(b.p_full);
+  }
+  // ---- epilogue: O / l -> bf16
+  float l;
+  {
+    float a0, a1, b0, b1;
+    unpack_f32x2(lacc0, a0, a1);
+    unpack_f32x2(lacc1, b0, b1);
+    l = (a0 + a1) + (b0 + b1);
+  }
+  k3_wait(b.o_full, 0);
+  tc_fence_after();
+  const int row = T.qb * 128 + i;
+  const bool valid = row < S;
+  const float inv = 1.f / l;
+  __nv_bfloat16* dst = out + ((size_t)T.h * S + row) * 128;
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    uint32_t r[32];
+    tmem_ld32_sync(tO + ch * 32, r);
+    uint32_t pk[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      pk[t] = pack_bf16(__uint_as_float(r[2 * t]) * inv, __uint_as_float(r[2 * t + 1]) * inv);
+    if (valid) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst + ch * 32);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) d4[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+    }
+  }
+  if (valid && lse) lse[(size_t)T.h * S + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
+  if (i == 0 && touched) atomicAdd(reinterpret_cast<unsigned long long*>(touched + T.h), (unsigned long long)T.n);
+}
+
+}  // namespace sa

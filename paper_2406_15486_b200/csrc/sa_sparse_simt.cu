@@ -25,7 +25,8 @@ __global__ void __launch_bounds__(128)
   float (*ks)[DP + 1] = reinterpret_cast<float (*)[DP + 1]>(sm_f);
   float (*vs)[DP + 1] = reinterpret_cast<float (*)[DP + 1]>(sm_f + kChunk * (DP + 1));
   float (*qs)[DP + 1] = reinterpret_cast<float (*)[DP + 1]>(sm_f + 2 * kChunk * (DP + 1));
-  const int item = order ? order[blockIdx.x] : (int)blockIdx.x;
+  const int item = order ? order[blockIdx.x] : (int)blockIdx.x;  // flattened unit list
+  if (item < 0) return;
   const int h = item / nb, qb = item - h * nb;
   const int n = kv_cnt[item];
   const int* list = kv_idx + (size_t)h * tri(nb) + tri(qb);
@@ -98,12 +99,12 @@ __global__ void __launch_bounds__(128)
 
 int launch_sparse_simt(const float* q, const float* k, const float* v, int S, int Hq, int Hkv, int d,
                        int blk, int group, int q_head0, const int* kv_cnt, const int* kv_idx,
-                       const int* order, float* out, float* lse, long long* touched,
+                       const int* order, int n_order, float* out, float* lse, long long* touched,
                        cudaStream_t st) {
   const int nb = ceil_div(S, blk);
   const int threads = blk < 32 ? 32 : blk;
   if (touched) cudaMemsetAsync(touched, 0, sizeof(long long) * Hq, st);
-  const dim3 grid(Hq * nb);
+  const dim3 grid(order ? n_order : Hq * nb);
 #define SA_SIMT_CASE(DPV)                                                                    \
   do {                                                                                       \
   cudaFuncSetAttribute(k3_simt<DPV>, cudaFuncAttributeMaxDynamicSharedMemorySize,               \

@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   unsigned char* sV = base + 2 * kTileBytes;
   K3Smem* sm = reinterpret_cast<K3Smem*>(base + 3 * kTileBytes);
 
-  const int item = P.order ? P.order[blockIdx.x] : (int)blockIdx.x;
+  const int item = P.order ? P.order[blockIdx.x] : (int)blockIdx.x;  // flattened unit list
+  if (item < 0) return;  // uniform per CTA, before any barrier or TMEM use
   const int h = item / P.nb, qb = item - h * P.nb;
   const int n = P.kv_cnt[item];
   const int* list = P.kv_idx + (size_t)h * tri(P.nb) + tri(qb);
@@ -412,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 }  // namespace
 
 int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq, int Hkv, int group,
-                     int q_head0, const int* kv_cnt, const int* kv_idx, const int* order, void* out,
+                     int q_head0, const int* kv_cnt, const int* kv_idx, const int* order, int n_order, void* out,
                      float* lse, long long* touched, cudaStream_t st) {
   CUtensorMap tq, tk, tv;
   if (!make_tmap_bf16_hsd(&tq, q, Hq, S, 128) || !make_tmap_bf16_hsd(&tk, k, Hkv, S, 128) ||
@@ -445,12 +446,13 @@ int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq,
     return e ? atoi(e) : 0;
   }();
   if (touched) cudaMemsetAsync(touched, 0, sizeof(long long) * Hq, st);
+  const int grid = order ? n_order : Hq * P.nb;
   switch (exp_mode) {
-    case 1: k3_tc<1><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
-    case 2: k3_tc<2><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
-    case 3: k3_tc<3><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
-    case 4: k3_tc<4><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
-    default: k3_tc<0><<<Hq * P.nb, kThreads, smem, st>>>(tq, tk, tv, P); break;
+    case 1: k3_tc<1><<<grid, kThreads, smem, st>>>(tq, tk, tv, P); break;
+    case 2: k3_tc<2><<<grid, kThreads, smem, st>>>(tq, tk, tv, P); break;
+    case 3: k3_tc<3><<<grid, kThreads, smem, st>>>(tq, tk, tv, P); break;
+    case 4: k3_tc<4><<<grid, kThreads, smem, st>>>(tq, tk, tv, P); break;
+    default: k3_tc<0><<<grid, kThreads, smem, st>>>(tq, tk, tv, P); break;
   }
   return check_launch("sparse_forward tcgen05");
 }

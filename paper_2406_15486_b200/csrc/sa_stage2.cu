@@ -13,7 +13,7 @@
 //            ({qb-ob-1, qb-ob} clipped to [0, qb]) of the 1-2 chunks whose
 //            region covers qb, and the diagonal, as an ascending list.
 // k2_full    dense causal mask (the dense comparison row).
-// k2_sched   longest-first order of (head, query block) work items.
+// k2_units   stage-3 work units (two items of one KV head), longest-first.
 #include <algorithm>
 
 #include "sa_internal.h"
@@ -226,40 +226,50 @@ __global__ void k2_full(int Hq, int nb, int* __restrict__ kv_cnt, int* __restric
   if (threadIdx.x == 0) kv_cnt[item] = qb + 1;
 }
 
-// Counting sort of work items by descending block count, one CTA per KV
-// group: the q heads of a group are contiguous, so its items are the
-// contiguous range [seg_lo, seg_hi) of h*nb + qb, and sorting each group's
-// range in place yields a group-major, longest-first order.  Group-major keeps
-// one KV head's K/V (64 MiB at 128K) resident in L2 while its items run.
-__global__ void __launch_bounds__(1024) k2_sched(const int* __restrict__ kv_cnt, int Hq, int nb, int group,
-                                                 int q_head0, int* __restrict__ order) {
-  extern __shared__ int hist[];  // [nb + 2]
-  // heads of local kv group blockIdx.x
-  const int g_first = q_head0 / group;
-  int h_lo = max(0, (g_first + (int)blockIdx.x) * group - q_head0);
-  int h_hi = min(Hq, (g_first + (int)blockIdx.x + 1) * group - q_head0);
-  if (h_lo >= h_hi) return;
-  const int lo = h_lo * nb, hi = h_hi * nb;
-  for (int i = threadIdx.x; i < nb + 2; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
-  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    int c = min(max(kv_cnt[i], 0), nb);
-    atomicAdd(hist + c, 1);
+// Stage-3 work units (sa_internal.h: two items of one KV head per unit),
+// counting-sorted by descending cost kv_cnt[a] + kv_cnt[b], one CTA per local
+// KV group.  Group-major keeps one KV head's K/V (64 MiB at 128K) resident in
+// L2 while its units run; longest-first inside a group evens out the tail.
+__global__ void __launch_bounds__(1024) k2_units(const int* __restrict__ kv_cnt, int Hq, int nb, int group,
+                                                 int q_head0, int* __restrict__ units) {
+  extern __shared__ int hist[];  // [2 * nb + 2]
+  int h_lo, h_hi;
+  kv_group_heads(blockIdx.x, Hq, group, q_head0, h_lo, h_hi);
+  const int nh = h_hi - h_lo;
+  if (nh <= 0) return;
+  int base = 0;  // units of the groups before this one
+  for (int g = 0; g < (int)blockIdx.x; ++g) {
+    int lo, hi;
+    kv_group_heads(g, Hq, group, q_head0, lo, hi);
+    base += units_of_group(hi - lo, nb);
   }
+  const int nu = units_of_group(nh, nb);
+  const int nbins = 2 * nb + 2;
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  auto cost = [&](int u) {
+    int a, b;
+    unit_items(u, h_lo, nh, nb, a, b);
+    const int c = max(kv_cnt[a], 0) + (b >= 0 ? max(kv_cnt[b], 0) : 0);
+    return min(c, nbins - 1);
+  };
+  for (int u = threadIdx.x; u < nu; u += blockDim.x) atomicAdd(hist + cost(u), 1);
   __syncthreads();
   if (threadIdx.x == 0) {
-    int run = lo;  // descending: bin nb first
-    for (int c = nb; c >= 0; --c) {
+    int run = base;  // descending cost
+    for (int c = nbins - 1; c >= 0; --c) {
       const int v = hist[c];
       hist[c] = run;
       run += v;
     }
   }
   __syncthreads();
-  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    int c = min(max(kv_cnt[i], 0), nb);
-    const int slot = atomicAdd(hist + c, 1);
-    order[slot] = i;
+  for (int u = threadIdx.x; u < nu; u += blockDim.x) {
+    const int slot = atomicAdd(hist + cost(u), 1);
+    int a, b;
+    unit_items(u, h_lo, nh, nb, a, b);
+    units[2 * slot] = a;
+    units[2 * slot + 1] = b;
   }
 }
 
@@ -322,12 +332,11 @@ int launch_full(int Hq, int nb, int* kv_cnt, int* kv_idx, cudaStream_t st) {
   return check_launch("sa_full_mask");
 }
 
-int launch_sched(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* order, cudaStream_t st) {
-  const size_t smem = (size_t)(nb + 2) * 4;
+int launch_sched(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* units, cudaStream_t st) {
+  const size_t smem = (size_t)(2 * nb + 2) * 4;
   if (smem > 200 * 1024) return fail(SA_ERR_UNSUPPORTED, "sa_schedule: nb too large");
-  cudaFuncSetAttribute(k2_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int n_groups = (q_head0 + Hq - 1) / group - q_head0 / group + 1;
-  k2_sched<<<n_groups, 1024, smem, st>>>(kv_cnt, Hq, nb, group, q_head0, order);
+  cudaFuncSetAttribute(k2_units, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k2_units<<<n_local_kv(Hq, group, q_head0), 1024, smem, st>>>(kv_cnt, Hq, nb, group, q_head0, units);
   return check_launch("sa_schedule");
 }
 

@@ -20,6 +20,7 @@ exact stage 1 for every pair; "never" skips the guard.
 
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -54,6 +55,22 @@ def _workspace(b: HeadBatch, blk: int, cn: int) -> torch.Tensor:
         ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=b.q.device)
         _WS_CACHE[key] = ws
     return ws
+
+
+@contextlib.contextmanager
+def private_workspace(b: HeadBatch, blk: int, cn: int):
+    """Within the block, stage calls on this geometry use a fresh workspace
+    that is NOT shared with later calls (CUDA-graph capture: the graph keeps
+    the pointer, so it must own the buffer).  Yields the workspace tensor."""
+    key = (b.q.device, b.S, b.Hq, b.Hkv, b.d, blk, cn, b.dtype_code)
+    saved = _WS_CACHE.pop(key, None)
+    ws = _workspace(b, blk, cn)
+    try:
+        yield ws
+    finally:
+        _WS_CACHE.pop(key, None)
+        if saved is not None:
+            _WS_CACHE[key] = saved
 
 
 def as_batch(heads, dtype=None) -> HeadBatch:
