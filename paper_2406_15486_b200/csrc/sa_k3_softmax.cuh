@@ -32,6 +32,34 @@ struct K3TileBars {
 
 constexpr float kK3RescaleThreshold = 8.0f;  // log2 units
 
+// Cycle accounting (build with -DSA_K3_PROF=1, read with sa_debug_k3s_profile):
+// slots 0-3 softmax (wait S, pass 1, rescale, pass 2), 4 epilogue wait,
+// 5-9 issuer (wait P part, P full, V, K, Q), 10-11 producer (wait K, V empty),
+// 12 issuer loop total, 13 blocks processed.
+#ifndef SA_K3_PROF
+#define SA_K3_PROF 0
+#endif
+__device__ unsigned long long g_k3s_prof[16];
+struct K3Prof {
+#if SA_K3_PROF
+  long long acc[16] = {0};
+  long long t0 = 0;
+  __device__ __forceinline__ void start() { t0 = clock64(); }
+  __device__ __forceinline__ void stop(int slot) { acc[slot] += clock64() - t0; }
+  __device__ __forceinline__ void add(int slot, long long v) { acc[slot] += v; }
+  __device__ __forceinline__ void flush(bool leader) {
+    if (leader)
+      for (int k = 0; k < 16; ++k)
+        if (acc[k]) atomicAdd(&g_k3s_prof[k], (unsigned long long)acc[k]);
+  }
+#else
+  __device__ __forceinline__ void start() {}
+  __device__ __forceinline__ void stop(int) {}
+  __device__ __forceinline__ void add(int, long long) {}
+  __device__ __forceinline__ void flush(bool) {}
+#endif
+};
+
 // Fraction of off-diagonal exponentials computed by the FMA-pipe polynomial:
 // SA_K3_POLY n -> n/4 (build-time experiment knob; production 1).
 #ifndef SA_K3_POLY
@@ -41,6 +69,10 @@ constexpr float kK3RescaleThreshold = 8.0f;  // log2 units
 // 2 = no exponentials (P = the scaled score, finite garbage).
 #ifndef SA_K3_EXP
 #define SA_K3_EXP 0
+#endif
+// Single-read fast path for off-diagonal blocks (see k3_softmax_tile).
+#ifndef SA_K3_FAST
+#define SA_K3_FAST 1
 #endif
 
 
@@ -54,11 +86,75 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
   const uint64_t sl2x2 = f32x2(sl2, sl2);
   float m_ref = -INFINITY;
   uint64_t lacc0 = f32x2(0.f, 0.f), lacc1 = f32x2(0.f, 0.f);
+  K3Prof pf;
   for (int j = 0; j < T.n; ++j) {
     const int kb = __ldg(T.list + j);
     const bool diag = kb == T.qb;  // warp-uniform
+    pf.start();
     k3_wait(b.s_full, j & 1);
+    pf.stop(0);
+    pf.start();
     tc_fence_after();
+#if SA_K3_FAST
+    // ---- fast path (off-diagonal blocks after the first): ONE read of S.
+    // Exponentials are taken against the running max m_ref, which the lazy
+    // rescale already allows to trail the true max by up to 2^8; the block's
+    // max is checked on the way and the packed P is held in registers until
+    // the check passes.  If any row's max exceeds m_ref + 8 (rare once the
+    // heavy columns have been seen) S is still intact in TMEM and the block
+    // falls through to the two-pass path below.
+    if (j > 0 && !diag && SA_K3_EXP == 0) {
+      const uint64_t negm = f32x2(-m_ref, -m_ref);
+      uint32_t pk[64];
+      uint64_t bacc0 = f32x2(0.f, 0.f), bacc1 = f32x2(0.f, 0.f);
+      float ymax = -INFINITY;
+      {
+        uint32_t buf[2][32];
+        tmem_ld32(tS, buf[0]);
+        tmem_ld_wait_regs(buf[0]);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t(&r)[32] = buf[ch & 1];
+          if (ch < 3) tmem_ld32(tS + (ch + 1) * 32, buf[(ch + 1) & 1]);
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            float y0, y1;
+            unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm),
+                         y0, y1);
+            ymax = fmax3(ymax, y0, y1);
+            const uint64_t pp = ((t & 3) >= 4 - SA_K3_POLY) ? ex2_poly2(y0, y1) : f32x2(ex2(y0), ex2(y1));
+            if (t & 1)
+              bacc1 = fadd2(bacc1, pp);
+            else
+              bacc0 = fadd2(bacc0, pp);
+            float p0, p1;
+            unpack_f32x2(pp, p0, p1);
+            pk[ch * 16 + t] = pack_bf16(p0, p1);
+          }
+          if (ch < 3) tmem_ld_wait_regs(buf[(ch + 1) & 1]);
+        }
+      }
+      if (!__any_sync(0xffffffffu, ymax > kK3RescaleThreshold)) {
+        lacc0 = fadd2(lacc0, bacc0);
+        lacc1 = fadd2(lacc1, bacc1);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t(&q)[16] = *reinterpret_cast<uint32_t(*)[16]>(&pk[ch * 16]);
+          tmem_st16(tS + ch * 16, q);
+          if (ch == 2) {  // keys 0..95 of P are in TMEM: let the PV MMA start
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(b.p_part);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(b.p_full);
+        pf.stop(3);
+        continue;
+      }
+    }
+#endif
     if (SA_K3_EXP == 1) {
       tc_fence_before();
       mbar_arrive(b.p_part);
@@ -91,6 +187,8 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
       }
     }
     const float mxs = fmax3(fmaxf(ma, mb), mc, md) * sl2;
+    pf.stop(1);
+    pf.start();
     // tcgen05.ld/st are warp-collective: rescale decision per warp.  O is
     // stable here: PV(j-1) completed before S(j) did (in-order tensor pipe).
     if (__any_sync(0xffffffffu, mxs > m_ref + kK3RescaleThreshold)) {
@@ -117,6 +215,8 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
       }
       m_ref = m_new;
     }
+    pf.stop(2);
+    pf.start();
     // ---- pass 2: P = exp2(s*log2e/sqrt(d) - m) -> bf16 over S, row sum
     const uint64_t negm = f32x2(-m_ref, -m_ref);
     {
@@ -174,6 +274,7 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
     tmem_st_wait();
     tc_fence_before();
     mbar_arrive(b.p_full);
+    pf.stop(3);
   }
   // ---- epilogue: O / l -> bf16
   float l;
@@ -183,7 +284,10 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
     unpack_f32x2(lacc1, b0, b1);
     l = (a0 + a1) + (b0 + b1);
   }
+  pf.start();
   k3_wait(b.o_full, 0);
+  pf.stop(4);
+  pf.flush(lane_id() == 0);
   tc_fence_after();
   const int row = T.qb * 128 + i;
   const bool valid = row < S;

@@ -166,20 +166,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       UnionWalk w{T[0].list, T[1].list, T[0].n, T[1].n, 0, 0};
       int kb;
       bool inA, inB;
+      K3Prof pf;
       for (int t = 0; w.next(kb, inA, inB); ++t) {
         const int s = t & 1;
         const int key0 = kb * 128;
+        pf.start();
         if (t >= 2) k3_wait(&sm->k_empty[s], ((t - 2) >> 1) & 1);
+        pf.stop(10);
         mbar_expect_tx(&sm->k_full[s], kTileBytes);
         unsigned char* sK = sK0 + s * kTileBytes;
         tma_load_3d_hint(sK, &tm_k, &sm->k_full[s], 0, key0, kvh, keep);
         tma_load_3d_hint(sK + kBoxBytes, &tm_k, &sm->k_full[s], 64, key0, kvh, keep);
+        pf.start();
         if (t >= 2) k3_wait(&sm->v_empty[s], ((t - 2) >> 1) & 1);
+        pf.stop(11);
         mbar_expect_tx(&sm->v_full[s], kTileBytes);
         unsigned char* sV = sV0 + s * kTileBytes;
         tma_load_3d_hint(sV, &tm_v, &sm->v_full[s], 0, key0, kvh, keep);
         tma_load_3d_hint(sV + kBoxBytes, &tm_v, &sm->v_full[s], 64, key0, kvh, keep);
       }
+      pf.flush(true);
     }
   } else if (warp == 1) {
     const uint32_t q_addr[2] = {smem_u32(sQ[0]), smem_u32(sQ[1])};
@@ -187,6 +193,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     int n_s[2] = {0, 0};      // S MMAs issued per item
     int n_pv[2] = {0, 0};     // PV MMAs issued per item
     int pend[2] = {-1, -1};   // union step whose PV is still to be issued
+    K3Prof pf;
+#if SA_K3_PROF
+    const long long t_loop = clock64();
+#endif
     UnionWalk w{T[0].list, T[1].list, T[0].n, T[1].n, 0, 0};
     int kb;
     bool in[2];
@@ -195,8 +205,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_pv = [&](int x, int step) {
       const int j = n_pv[x];
       const int s = step & 1;
+      pf.start();
       k3_wait(&sm->p_part[x], j & 1);
+      pf.stop(5);
+      pf.start();
       k3_wait(&sm->v_full[s], (step >> 1) & 1);
+      pf.stop(7);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -205,7 +219,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                   (j > 0 || kk > 0) ? 1u : 0u);
       }
       __syncwarp();
+      pf.start();
       k3_wait(&sm->p_full[x], j & 1);
+      pf.stop(6);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -219,7 +235,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     while (w.next(kb, in[0], in[1])) {
       const int s = t & 1;
+      pf.start();
       k3_wait(&sm->k_full[s], (t >> 1) & 1);
+      pf.stop(8);
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
         if (pend[x] >= 0) {
@@ -227,7 +245,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           pend[x] = -1;
         }
         if (in[x]) {
+          pf.start();
           if (n_s[x] == 0) k3_wait(&sm->q_full[x], 0);
+          pf.stop(9);
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
@@ -253,6 +273,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int x = 0; x < 2; ++x)
       if (pend[x] >= 0) issue_pv(x, pend[x]);
+#if SA_K3_PROF
+    pf.add(12, clock64() - t_loop);
+    pf.add(13, T[0].n + T[1].n);
+#endif
+    pf.flush(lane_id() == 0);
   } else if (warp >= 4) {
     const int x = warp < 8 ? 0 : 1;
     const K3Tile Tx = x ? T[1] : T[0];  // select, not a dynamically indexed (local-memory) array
@@ -303,3 +328,12 @@ int launch_sparse_share(const void* q, const void* k, const void* v, int S, int 
 }
 
 }  // namespace sa
+
+extern "C" int sa_debug_k3s_profile(unsigned long long* out16, int reset) {
+  cudaMemcpyFromSymbol(out16, sa::g_k3s_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(sa::g_k3s_prof, z, sizeof(z));
+  }
+  return 0;
+}
