@@ -62,12 +62,12 @@ int check_launch(const char* what) {
   return SA_OK;
 }
 
-bool make_tmap_bf16_hsd(CUtensorMap* map, const void* base, int H, int S, int d) {
+bool make_tmap_bf16_hsd(CUtensorMap* map, const void* base, int H, int S, int d, int box_rows) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)S, (cuuint64_t)H};
   const cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)S * d * 2};
-  const cuuint32_t box[3] = {64, 128, 1};
+  const cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -217,8 +217,12 @@ int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, in
   if (dtype == SA_BF16) {
     static const int impl = [] {
       const char* e = getenv("SA_K3_IMPL");
-      return (e && e[0] == 's') ? 1 : 0;  // "single": one item per CTA, two CTAs per SM (no K/V sharing)
+      if (e && e[0] == 's') return 1;  // "single": one item per CTA, two CTAs per SM (no K/V sharing)
+      if (e && e[0] == 'p') return 2;  // "pair": units over SM pairs (cta_group::2)
+      return 0;                        // "share": units in one CTA
     }();
+    if (impl == 2)
+      return launch_sparse_pair(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse, touched, st);
     if (impl == 1)
       return launch_sparse_tc(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, n_order, out, lse,
                               touched, st);

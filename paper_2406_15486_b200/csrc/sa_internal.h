@@ -61,8 +61,8 @@ int launch_sparse_simt(const float* q, const float* k, const float* v, int S, in
                        const int* kv_idx, const int* order, int n_order, float* out, float* lse,
                        long long* touched, cudaStream_t st);
 
-// TMA descriptor for a contiguous [H][S][d] bf16 tensor, box {64, 128, 1}, 128B swizzle.
-bool make_tmap_bf16_hsd(CUtensorMap* map, const void* base, int H, int S, int d);
+// TMA descriptor for a contiguous [H][S][d] bf16 tensor, box {64, box_rows, 1}, 128B swizzle.
+bool make_tmap_bf16_hsd(CUtensorMap* map, const void* base, int H, int S, int d, int box_rows = 128);
 
 __host__ __device__ inline int kv_head_of(int h, int group, int q_head0) {
   return (q_head0 + h) / group - q_head0 / group;
@@ -108,6 +108,9 @@ __host__ __device__ inline int n_units(int Hq, int nb, int group, int q_head0) {
   return total;
 }
 
+int launch_sparse_pair(const void* q, const void* k, const void* v, int S, int Hq, int Hkv, int group,
+                       int q_head0, const int* kv_cnt, const int* kv_idx, const int* units, void* out,
+                       float* lse, long long* touched, cudaStream_t st);
 int launch_sparse_share(const void* q, const void* k, const void* v, int S, int Hq, int Hkv, int group,
                         int q_head0, const int* kv_cnt, const int* kv_idx, const int* units, void* out,
                         float* lse, long long* touched, cudaStream_t st);

@@ -25,12 +25,16 @@ struct K3Tile {
 
 struct K3TileBars {
   uint64_t* s_full;  // S(j) landed in TMEM           (tcgen05.commit)
-  uint64_t* p_part;  // P(j) keys 0..95 in TMEM        (128 arrivals)
-  uint64_t* p_full;  // P(j) complete                  (128 arrivals)
+  uint64_t* p_part;  // P(j) keys 0..95 in TMEM        (128 arrivals; pair mode: 1 per CTA)
+  uint64_t* p_full;  // P(j) complete                  (128 arrivals; pair mode: 1 per CTA)
   uint64_t* o_full;  // last PV done                   (tcgen05.commit)
 };
 
 constexpr float kK3RescaleThreshold = 8.0f;  // log2 units
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 
 // Cycle accounting (build with -DSA_K3_PROF=1, read with sa_debug_k3s_profile):
 // slots 0-3 softmax (wait S, pass 1, rescale, pass 2), 4 epilogue wait,
@@ -39,7 +43,7 @@ constexpr float kK3RescaleThreshold = 8.0f;  // log2 units
 #ifndef SA_K3_PROF
 #define SA_K3_PROF 0
 #endif
-__device__ unsigned long long g_k3s_prof[16];
+static __device__ unsigned long long g_k3s_prof[16];  // one copy per kernel translation unit
 struct K3Prof {
 #if SA_K3_PROF
   long long acc[16] = {0};
@@ -76,9 +80,21 @@ struct K3Prof {
 #endif
 
 
+// Pair mode (cta_group::2 kernel): the tile walks the ascending UNION of its own
+// block list and its partner's (one 256-row MMA covers both tiles); on steps
+// outside its own list it only writes P = 0 for its rows.  The P-ready
+// arrivals go to the pair leader's barriers (cluster addresses).
+struct K3PairCtx {
+  const int* other_list;
+  int other_n;
+  uint32_t p_part_cl, p_full_cl;  // the leader's P barriers (cluster addresses)
+  bool remote;                    // this CTA is the peer: arrive remotely
+};
+
+template <bool kPair>
 __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBars& b, uint32_t tS0,
                                                 uint32_t tO0, int quad, int S, __nv_bfloat16* out,
-                                                float* lse, long long* touched) {
+                                                float* lse, long long* touched, const K3PairCtx pc = {}) {
   const int i = quad * 32 + lane_id();  // query row within the tile
   const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
   const uint32_t tS = tS0 + lane_off, tO = tO0 + lane_off;
@@ -87,14 +103,64 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
   float m_ref = -INFINITY;
   uint64_t lacc0 = f32x2(0.f, 0.f), lacc1 = f32x2(0.f, 0.f);
   K3Prof pf;
-  for (int j = 0; j < T.n; ++j) {
-    const int kb = __ldg(T.list + j);
+  // P-ready arrivals.  Single-SM kernels: every softmax thread arrives on the
+  // CTA's own barrier (count 128).  Pair mode: the tile's 128 softmax threads
+  // meet at a named barrier (each has waited for and fenced its own TMEM
+  // stores first), then ONE thread arrives on the leader CTA's barrier (count
+  // 2: one per CTA) -- a remote cluster-scope arrive per thread stalls every
+  // warp, one per CTA does not.
+  auto arrive_on = [&](uint64_t* local, uint32_t cl) {
+    if (kPair) {
+      named_bar_sync(1, 128);
+      if (quad == 0 && lane_id() == 0) {
+        if (pc.remote)
+          mbar_arrive_cluster(cl);
+        else
+          mbar_arrive(local);
+      }
+    } else {
+      mbar_arrive(local);
+    }
+  };
+  auto arrive_part = [&]() { arrive_on(b.p_part, pc.p_part_cl); };
+  auto arrive_full = [&]() { arrive_on(b.p_full, pc.p_full_cl); };
+  int ia = 0, ib = 0;  // union walk (pair mode)
+  int jj = 0;          // own blocks processed so far
+  for (int j = 0;; ++j) {
+    int kb;
+    bool mine = true;
+    if (kPair) {
+      if (ia >= T.n && ib >= pc.other_n) break;
+      const int ka = ia < T.n ? __ldg(T.list + ia) : 0x7fffffff;
+      const int kc = ib < pc.other_n ? __ldg(pc.other_list + ib) : 0x7fffffff;
+      kb = min(ka, kc);
+      mine = ka == kb;
+      ia += mine;
+      ib += kc == kb;
+    } else {
+      if (j >= T.n) break;
+      kb = __ldg(T.list + j);
+    }
     const bool diag = kb == T.qb;  // warp-uniform
     pf.start();
     k3_wait(b.s_full, j & 1);
     pf.stop(0);
     pf.start();
     tc_fence_after();
+    if (kPair && !mine) {  // not this tile's block: its rows contribute P = 0
+      uint32_t z[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) z[t] = 0u;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) tmem_st16(tS + ch * 16, z);
+      tmem_st_wait();
+      tc_fence_before();
+      arrive_part();
+      arrive_full();
+      continue;
+    }
+    const bool first = jj == 0;
+    ++jj;
 #if SA_K3_FAST
     // ---- fast path (off-diagonal blocks after the first): ONE read of S.
     // Exponentials are taken against the running max m_ref, which the lazy
@@ -103,7 +169,7 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
     // the check passes.  If any row's max exceeds m_ref + 8 (rare once the
     // heavy columns have been seen) S is still intact in TMEM and the block
     // falls through to the two-pass path below.
-    if (j > 0 && !diag && SA_K3_EXP == 0) {
+    if (!first && !diag && SA_K3_EXP == 0) {
       const uint64_t negm = f32x2(-m_ref, -m_ref);
       uint32_t pk[64];
       uint64_t bacc0 = f32x2(0.f, 0.f), bacc1 = f32x2(0.f, 0.f);
@@ -144,12 +210,12 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
           if (ch == 2) {  // keys 0..95 of P are in TMEM: let the PV MMA start
             tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(b.p_part);
+            arrive_part();
           }
         }
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(b.p_full);
+        arrive_full();
         pf.stop(3);
         continue;
       }
@@ -157,8 +223,8 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
 #endif
     if (SA_K3_EXP == 1) {
       tc_fence_before();
-      mbar_arrive(b.p_part);
-      mbar_arrive(b.p_full);
+      arrive_part();
+      arrive_full();
       continue;
     }
     // ---- pass 1: row max (four FMNMX3 chains)
@@ -193,7 +259,7 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
     // stable here: PV(j-1) completed before S(j) did (in-order tensor pipe).
     if (__any_sync(0xffffffffu, mxs > m_ref + kK3RescaleThreshold)) {
       const float m_new = fmaxf(m_ref, mxs);
-      if (j > 0) {
+      if (!first) {
         const float f = ex2(m_ref - m_new);
         const uint64_t f2 = f32x2(f, f);
         lacc0 = fmul2(lacc0, f2);
@@ -266,16 +332,17 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
         if (ch == 2) {  // keys 0..95 of P are in TMEM: let the PV MMA start
           tmem_st_wait();
           tc_fence_before();
-          mbar_arrive(b.p_part);
+          arrive_part();
         }
         if (ch < 3) tmem_ld_wait_regs(buf[(ch + 1) & 1]);
       }
     }
     tmem_st_wait();
     tc_fence_before();
-    mbar_arrive(b.p_full);
+    arrive_full();
     pf.stop(3);
   }
+  if (kPair && T.n == 0) return;  // CTA without an item: its rows only padded the pair MMA
   // ---- epilogue: O / l -> bf16
   float l;
   {

@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const K3Tile Tx = x ? T[1] : T[0];  // select, not a dynamically indexed (local-memory) array
     if (Tx.n > 0) {
       const K3TileBars b{&sm->s_full[x], &sm->p_part[x], &sm->p_full[x], &sm->o_full[x]};
-      k3_softmax_tile(Tx, b, x ? tS[1] : tS[0], x ? tO[1] : tO[0], warp & 3, P.S, P.out, P.lse, P.touched);
+      k3_softmax_tile<false>(Tx, b, x ? tS[1] : tS[0], x ? tO[1] : tO[0], warp & 3, P.S, P.out, P.lse, P.touched);
     }
   }
   tc_fence_before();
