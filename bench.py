@@ -363,7 +363,7 @@ def main():
             traffic = json.load(open(tpath)).get("bytes_per_launch")
         except Exception:
             traffic = None
-    roof = {"bound": "tensor", "kernel": "k3_tc (stage-3 sparse prefill)", "achieved": round(achieved, 2),
+    roof = {"bound": "tensor", "kernel": "k3_share (stage-3 sparse prefill, K/V-sharing units)", "achieved": round(achieved, 2),
             "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": round(achieved / pk["bf16_tflops"], 4),
             "frac_of_sustained": round(achieved / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]), 4),
             "peak_source": pk_kind, "traffic": traffic,

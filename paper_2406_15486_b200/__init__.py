@@ -17,6 +17,7 @@ from .heads import AttentionHead, HeadBatch, HeadSet, check_finite
 from .masks import BlockMask, ChunkSelection, SelectedIndices
 from .pipeline import (ORACLE_CAP, HeadMetrics, MetricsReport, SampleAttentionResult, dense_attention,
                        run_pipeline, sample_attention)
+from . import tensor_io
 from .graph import SampleAttentionGraph
 from .streaming import sample_attention_host
 from .stages import (GUARD_EPS, ChunkScores, FlopReport, ReducedScores, SampledScores, arg_topk, block_reduce,

@@ -360,6 +360,9 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
   const bool valid = row < S;
   const float inv = 1.f / l;
   __nv_bfloat16* dst = out + ((size_t)T.h * S + row) * 128;
+  // the output streams through L2 once: mark it evict-first so it does not push
+  // out the K/V of the KV head the other units are still reading
+  const uint64_t stream_out = policy_evict_first();
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
     uint32_t r[32];
@@ -371,7 +374,8 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
     if (valid) {
       uint4* d4 = reinterpret_cast<uint4*>(dst + ch * 32);
 #pragma unroll
-      for (int t = 0; t < 4; ++t) d4[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+      for (int t = 0; t < 4; ++t)
+        st_global_v4_hint(d4 + t, make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]), stream_out);
     }
   }
   if (valid && lse) lse[(size_t)T.h * S + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;

@@ -156,12 +156,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      const uint64_t keep = policy_evict_last();
+      const uint64_t keep = policy_evict_last(), once = policy_evict_first();
       for (int x = 0; x < 2; ++x)
-        if (T[x].n > 0) {
+        if (T[x].n > 0) {  // Q is read once: evict-first, K/V are re-read by every unit of the KV head: evict-last
           mbar_expect_tx(&sm->q_full[x], kTileBytes);
-          tma_load_3d(sQ[x], &tm_q, &sm->q_full[x], 0, T[x].qb * 128, T[x].h);
-          tma_load_3d(sQ[x] + kBoxBytes, &tm_q, &sm->q_full[x], 64, T[x].qb * 128, T[x].h);
+          tma_load_3d_hint(sQ[x], &tm_q, &sm->q_full[x], 0, T[x].qb * 128, T[x].h, once);
+          tma_load_3d_hint(sQ[x] + kBoxBytes, &tm_q, &sm->q_full[x], 64, T[x].qb * 128, T[x].h, once);
         }
       UnionWalk w{T[0].list, T[1].list, T[0].n, T[1].n, 0, 0};
       int kb;
