@@ -92,8 +92,8 @@ Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int d
   off = align_up(off + 3 * rows * nb * sizeof(double));
   L.part3 = off;
   off = align_up(off + (size_t)Hq * cn * nb * 4 * sizeof(double));
-  L.sched = off;
-  off = align_up(off + (size_t)(nb + 2) * sizeof(int));
+  L.flag_list = off;
+  off = align_up(off + (size_t)(Hq * cn + 2) * sizeof(int));
   L.total = off;
   return L;
 }

@@ -35,7 +35,7 @@ struct Workspace {
   size_t rowstat;   // double [Hq*cn*blk][2]      (log2 max, sum) per sampled row
   size_t x_part;    // double [3][Hq*cn*blk*nb]   exact (A, B, m) per (row, key block)
   size_t part3;     // double [Hq*cn*nb][4]       (col, slash X-1, X, X+1) per key block
-  size_t sched;     // int    [nb + 2]
+  size_t flag_list; // int    [Hq*cn + 2]             compacted guard-flagged pairs: count, then indices
   size_t total;
 };
 Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int dtype);
@@ -46,11 +46,18 @@ int launch_stage1_exact(const Stage1Geom& g, const void* q, const void* k, int d
                         double* slash, cudaStream_t st);
 int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const int* only_flags,
                      char* ws, const Workspace& L, double* col, double* slash, cudaStream_t st);
-// rows' global max / sum, fold into part3, scatter into col / slash
+// rows' global max / sum, fold into part3, scatter into col / slash.  With
+// `only` (guard re-score), the flagged (head, chunk) pairs are first compacted
+// into ws + L.flag_list and every kernel loops over that list, so the grids
+// scale with the flagged pairs, not with Hq * chunk_n.
 template <typename TPlane, bool kLog2>
 int launch_fold(const Stage1Geom& g, const int* only, const TPlane* pa, const TPlane* pb,
                 const TPlane* pm, char* ws, const Workspace& L, double* col, double* slash,
                 cudaStream_t st);
+// compact the nonzero entries of only[0..n) into list = {count, i0, i1, ...}
+int launch_flag_compact(const int* only, int n, int* list, cudaStream_t st);
+// grid rows used for flagged-pair loops (enough to fill the GPU, bounded by the pair count)
+inline int flagged_grid_rows(int n_pairs) { return n_pairs < 32 ? n_pairs : 32; }
 
 int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq, int Hkv,
                      int group, int q_head0, const int* kv_cnt, const int* kv_idx,

@@ -154,20 +154,23 @@ __device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __rest
 }
 
 
-// One CTA per (head, chunk, key-block split).  For the guard's re-score
-// (`only` flags) every key block gets its own CTA so the few flagged pairs
-// spread over all SMs; CTAs of unflagged pairs exit at once.
+// One CTA per (key-block split, pair slot).  For the guard's re-score every
+// key block gets its own CTA so the few flagged pairs spread over all SMs, and
+// the pair slots loop over the compacted flagged list (L.flag_list).
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
-    xf_pass(const T* __restrict__ q, const T* __restrict__ k, Stage1Geom g, const int* __restrict__ only,
+    xf_pass(const T* __restrict__ q, const T* __restrict__ k, Stage1Geom g, const int* __restrict__ list,
             int kb_per_cta, double* __restrict__ pa, double* __restrict__ pb, double* __restrict__ pm) {
   extern __shared__ double smem_d[];
   double* qs = smem_d;                          // [kRows][kDChunk+1]
   double* ks = smem_d + kRows * (kDChunk + 1);  // [kKeys][kDChunk+1]
-  const int hc = blockIdx.y;
-  if (only && only[hc] == 0) return;
+  const int n_pairs = list ? list[0] : g.Hq * g.cn;
   const int kb0 = blockIdx.x * kb_per_cta;
-  xf_work(q, k, g, hc, kb0, kb0 + kb_per_cta, pa, pb, pm, qs, ks);
+  for (int f = blockIdx.y; f < n_pairs; f += gridDim.y) {  // uniform per CTA
+    const int hc = list ? list[1 + f] : f;
+    xf_work(q, k, g, hc, kb0, kb0 + kb_per_cta, pa, pb, pm, qs, ks);
+    __syncthreads();  // qs / ks are reused by the next pair
+  }
 }
 
 }  // namespace
@@ -177,11 +180,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // TPlane = float with log2-domain maxima (tensor-core partials) or double
 // with natural-log maxima (exact partials).
 template <typename TPlane, bool kLog2>
-__global__ void s1_rowfin(Stage1Geom g, const int* __restrict__ only, const TPlane* __restrict__ pa,
-                          const TPlane* __restrict__ pb, const TPlane* __restrict__ pm,
-                          double* __restrict__ rowstat) {
-  const int hc = blockIdx.y;
-  if (only && only[hc] == 0) return;
+__device__ __forceinline__ void rowfin_pair(Stage1Geom g, int hc, const TPlane* __restrict__ pa,
+                                            const TPlane* __restrict__ pb, const TPlane* __restrict__ pm,
+                                            double* __restrict__ rowstat) {
   const Win w = window_of(hc % g.cn, g.S, g.blk, g.itv);
   const int nr = w.se - w.ss;
   const int lane = threadIdx.x & 31, warps = blockDim.x >> 5;
@@ -203,15 +204,24 @@ __global__ void s1_rowfin(Stage1Geom g, const int* __restrict__ only, const TPla
   }
 }
 
+template <typename TPlane, bool kLog2>
+__global__ void s1_rowfin(Stage1Geom g, const int* __restrict__ list, const TPlane* __restrict__ pa,
+                          const TPlane* __restrict__ pb, const TPlane* __restrict__ pm,
+                          double* __restrict__ rowstat) {
+  const int n_pairs = list ? list[0] : g.Hq * g.cn;
+  for (int f = blockIdx.y; f < n_pairs; f += gridDim.y) {
+    const int hc = list ? list[1 + f] : f;
+    rowfin_pair<TPlane, kLog2>(g, hc, pa, pb, pm, rowstat);
+  }
+}
+
 // Per key block: fold the rows' normalised partial masses into part3
 // (col, slash X-1, X, X+1).  Thread per key block, rows in a fixed order.
 template <typename TPlane, bool kLog2>
-__global__ void s1_fold(Stage1Geom g, const int* __restrict__ only, const TPlane* __restrict__ pa,
-                        const TPlane* __restrict__ pb, const TPlane* __restrict__ pm,
-                        const double* __restrict__ rowstat, double* __restrict__ part3) {
-  __shared__ double s_w[kMaxSimtBlk][2];  // (M, 1/L) per row
-  const int hc = blockIdx.y;
-  if (only && only[hc] == 0) return;
+__device__ __forceinline__ void fold_pair(Stage1Geom g, int hc, const TPlane* __restrict__ pa,
+                                          const TPlane* __restrict__ pb, const TPlane* __restrict__ pm,
+                                          const double* __restrict__ rowstat, double* __restrict__ part3,
+                                          double (*s_w)[2]) {
   const Win w = window_of(hc % g.cn, g.S, g.blk, g.itv);
   const int nr = w.se - w.ss;
   for (int r = threadIdx.x; r < nr; r += blockDim.x) {
@@ -245,11 +255,24 @@ __global__ void s1_fold(Stage1Geom g, const int* __restrict__ only, const TPlane
   out[3] = s4[3];
 }
 
+template <typename TPlane, bool kLog2>
+__global__ void s1_fold(Stage1Geom g, const int* __restrict__ list, const TPlane* __restrict__ pa,
+                        const TPlane* __restrict__ pb, const TPlane* __restrict__ pm,
+                        const double* __restrict__ rowstat, double* __restrict__ part3) {
+  __shared__ double s_w[kMaxSimtBlk][2];  // (M, 1/L) per row
+  const int n_pairs = list ? list[0] : g.Hq * g.cn;
+  for (int f = blockIdx.y; f < n_pairs; f += gridDim.y) {
+    fold_pair<TPlane, kLog2>(g, list ? list[1 + f] : f, pa, pb, pm, rowstat, part3, s_w);
+    __syncthreads();  // s_w is reloaded for the next pair
+  }
+}
+
 // part3 -> col / slash
-__global__ void s1_finalize(Stage1Geom g, const int* __restrict__ only, const double* __restrict__ part3,
+__global__ void s1_finalize(Stage1Geom g, const int* __restrict__ list, const double* __restrict__ part3,
                             double* __restrict__ col, double* __restrict__ slash) {
-  const int hc = blockIdx.x;
-  if (only && only[hc] == 0) return;
+  const int n_pairs = list ? list[0] : g.Hq * g.cn;
+  if ((int)blockIdx.x >= n_pairs) return;
+  const int hc = list ? list[1 + blockIdx.x] : (int)blockIdx.x;
   const Win w = window_of(hc % g.cn, g.S, g.blk, g.itv);
   const int b0 = w.ss / g.blk;
   const double* p3 = part3 + (size_t)hc * g.nb * 4;
@@ -267,18 +290,43 @@ __global__ void s1_finalize(Stage1Geom g, const int* __restrict__ only, const do
   }
 }
 
+namespace {
+__global__ void k_flag_compact(const int* __restrict__ only, int n, int* __restrict__ list) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (only[i]) list[1 + atomicAdd(&cnt, 1)] = i;  // order is irrelevant: pairs are independent
+  __syncthreads();
+  if (threadIdx.x == 0) list[0] = cnt;
+}
+}  // namespace
+
+int launch_flag_compact(const int* only, int n, int* list, cudaStream_t st) {
+  k_flag_compact<<<1, 1024, 0, st>>>(only, n, list);
+  return check_launch("stage1 flag compaction");
+}
+
 template <typename TPlane, bool kLog2>
 int launch_fold(const Stage1Geom& g, const int* only, const TPlane* pa, const TPlane* pb,
                 const TPlane* pm, char* ws, const Workspace& L, double* col, double* slash,
                 cudaStream_t st) {
   double* rowstat = reinterpret_cast<double*>(ws + L.rowstat);
   double* part3 = reinterpret_cast<double*>(ws + L.part3);
-  s1_rowfin<TPlane, kLog2><<<dim3(16, g.Hq * g.cn), 256, 0, st>>>(g, only, pa, pb, pm, rowstat);
+  const int n_all = g.Hq * g.cn;
+  const int* list = nullptr;
+  int rows = n_all;
+  if (only) {  // the exact pass already compacted the flags for its own grid; rebuild (cheap) for the TC path
+    int* fl = reinterpret_cast<int*>(ws + L.flag_list);
+    if (int e = launch_flag_compact(only, n_all, fl, st)) return e;
+    list = fl;
+    rows = flagged_grid_rows(n_all);
+  }
+  s1_rowfin<TPlane, kLog2><<<dim3(16, rows), 256, 0, st>>>(g, list, pa, pb, pm, rowstat);
   if (int e = check_launch("stage1 rowfin")) return e;
-  s1_fold<TPlane, kLog2><<<dim3(ceil_div(g.nb, 128), g.Hq * g.cn), 128, 0, st>>>(g, only, pa, pb, pm,
-                                                                                rowstat, part3);
+  s1_fold<TPlane, kLog2><<<dim3(ceil_div(g.nb, 128), rows), 128, 0, st>>>(g, list, pa, pb, pm, rowstat, part3);
   if (int e = check_launch("stage1 fold")) return e;
-  s1_finalize<<<g.Hq * g.cn, 256, 0, st>>>(g, only, part3, col, slash);
+  s1_finalize<<<only ? n_all : n_all, 256, 0, st>>>(g, list, part3, col, slash);
   return check_launch("stage1 finalize");
 }
 
@@ -302,7 +350,14 @@ int run_exact(const Stage1Geom& g, const T* q, const T* k, const int* only, char
   double* pm = pb + plane;
   const long long work = (long long)g.Hq * g.cn * g.nb;
   const int kpc = only ? 1 : (int)std::max<long long>(2, std::min<long long>(32, work / (148LL * 4)));
-  xf_pass<T><<<dim3(ceil_div(g.nb, kpc), g.Hq * g.cn), kThreads, smem, st>>>(q, k, g, only, kpc, pa, pb, pm);
+  const int n_all = g.Hq * g.cn;
+  int* list = nullptr;
+  if (only) {
+    list = reinterpret_cast<int*>(ws + L.flag_list);
+    if (int e = launch_flag_compact(only, n_all, list, st)) return e;
+  }
+  const int rows = only ? flagged_grid_rows(n_all) : n_all;
+  xf_pass<T><<<dim3(ceil_div(g.nb, kpc), rows), kThreads, smem, st>>>(q, k, g, list, kpc, pa, pb, pm);
   if (int e = check_launch("stage1 exact pass")) return e;
   return launch_fold<double, false>(g, only, pa, pb, pm, ws, L, col, slash, st);
 }

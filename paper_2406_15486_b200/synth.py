@@ -57,7 +57,8 @@ def _smooth(gen, S: int, dims: int, sigma: int, device) -> torch.Tensor:
     ker = torch.exp(-(x ** 2) / (2.0 * sigma ** 2))
     ker = ker / ker.square().sum().sqrt()
     white = torch.randn((dims, 1, S + 2 * radius), generator=gen, device=device)
-    out = torch.nn.functional.conv1d(white, ker.view(1, 1, -1))  # [dims, 1, S]
+    with torch.backends.cudnn.flags(enabled=True, benchmark=False, deterministic=True):
+        out = torch.nn.functional.conv1d(white, ker.view(1, 1, -1))  # [dims, 1, S]
     return out[:, 0, :].T.contiguous()  # [S, dims]
 
 
@@ -110,7 +111,9 @@ def make_inputs(S: int, Hq: int, Hkv: int, d: int = 128, seed: int = 0, spec: Lo
         pos = torch.randint(0, int(S * 0.97), (spec.n_sinks,), generator=gen, device=device)
         pos[0] = 0
         bias = torch.zeros((S,), device=device)
-        bias[pos] = torch.tensor(sink_logit, device=device)
+        # colliding positions keep the larger logit (order-independent, so the
+        # generator is bit-deterministic; a plain index_put picks a random writer)
+        bias.scatter_reduce_(0, pos, torch.tensor(sink_logit, device=device), reduce="amax", include_self=False)
         k[:, n_noise] = bias * rd
         t0 = _smooth(gen, S, _TOPIC_DIMS, spec.band_sigma, device)
         t1 = _smooth(gen, S + slash_off, _TOPIC_DIMS, spec.band_sigma, device)

@@ -16,6 +16,7 @@ name the first bad element when that scan fails.
 from __future__ import annotations
 
 import struct
+import warnings
 
 import numpy as np
 import torch
@@ -111,7 +112,9 @@ def load_tensors_device(path, device=None, dtype=torch.bfloat16) -> HeadBatch:
     mm = np.memmap(path, dtype=np.uint8, mode="r")
     n, S, d, payload = _parse(path, memoryview(mm))
     dev = torch.device(device or "cuda")
-    host = torch.from_numpy(np.asarray(mm[payload:]).view("<f4").reshape(n, 3, S, d))
+    with warnings.catch_warnings():  # the map is read-only; torch only reads it for the copy
+        warnings.simplefilter("ignore", UserWarning)
+        host = torch.from_numpy(np.asarray(mm[payload:]).view("<f4").reshape(n, 3, S, d))
     cube = host.to(dev)  # fp32, one H2D copy
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     _lib.call("sa_check_finite", cube.data_ptr(), _lib.SA_FP32, cube.numel(), flag.data_ptr(),
