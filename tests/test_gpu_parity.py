@@ -289,3 +289,31 @@ def test_graph_executor_matches_eager(sa):
     g.replay()
     with pytest.raises(sa.InputError):
         g.check()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("Hq,Hkv,world", [(32, 2, 8), (32, 2, 4), (8, 8, 2), (6, 2, 2)])
+def test_head_shards_match_full_batch(sa, Hq, Hkv, world):
+    """Every rank's shard (q_head0 / group through the C ABI, work units built
+    per shard, odd heads pairing adjacent query blocks) reproduces its slice of
+    the unsharded batch bit for bit -- the N-GPU bench path on one GPU."""
+    import torch
+
+    from paper_2406_15486_b200 import synth
+    from paper_2406_15486_b200.parallel import shard_heads
+
+    S, group = 4096, Hq // Hkv
+    q, k, v, _ = synth.make_inputs(S, Hq, Hkv, 128, seed=5, device="cuda")
+    full, res = sa.sample_attention(q, k, v, alpha=0.95, chunk_n=2, group=group)
+    for r in range(world):
+        s = shard_heads(Hq, Hkv, world, r)
+        qs = q[s.q_heads[0]: s.q_heads[-1] + 1].contiguous()
+        ks = k[s.kv_heads[0]: s.kv_heads[-1] + 1].contiguous()
+        vs = v[s.kv_heads[0]: s.kv_heads[-1] + 1].contiguous()
+        o, rs = sa.sample_attention(qs, ks, vs, alpha=0.95, chunk_n=2, group=group, q_head0=s.q_head0)
+        g = sa.SampleAttentionGraph(qs, ks, vs, alpha=0.95, chunk_n=2, group=group, q_head0=s.q_head0)
+        og = g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(o, full[s.q_heads[0]: s.q_heads[-1] + 1])
+        assert torch.equal(og, o)
+        assert torch.equal(rs.mask.kv_cnt, res.mask.kv_cnt[s.q_heads[0]: s.q_heads[-1] + 1])

@@ -68,3 +68,30 @@ def test_determinism_at_scale(sa):
     assert torch.equal(o1, o2)
     assert torch.equal(r1.mask.kv_cnt, r2.mask.kv_cnt)
     assert np.array_equal(r1.mask.to_dense(), r2.mask.to_dense())  # padded CSR tails are scratch
+
+
+def test_selection_matches_oracle_at_1m(sa):
+    """C5 scale (S = 1M, the per-GPU share of the 8-GPU run: 4 q heads on one
+    KV head): every head's selected column / slash index sets are identical
+    to the oracle's on the same bf16 inputs; the merged rows of a few query
+    blocks are checked against the reference's merge rule."""
+    from paper_2406_15486_b200 import synth
+    S, Hq, Hkv = 1 << 20, 4, 1
+    q, k, v, _ = synth.make_inputs(S, Hq, Hkv, seed=0, device="cuda")
+    out, res = sa.sample_attention(q, k, v, alpha=0.95, chunk_n=1)
+    torch.cuda.synchronize()
+    sels = res.mask.selections()
+    plan = O.plan_chunks(S, 1, 128)
+    kh = k[0].double().cpu().numpy()
+    for h in range(Hq):
+        samples = O.sampled_probs(q[h].double().cpu().numpy(), kh, plan)
+        cols, slashes, _ = O.block_reduce(samples, S, 128)
+        ref = O.select(cols, slashes, 0.95, 0.95)
+        assert [(c.i_c, c.i_s) for c in sels[h].chunks] == [(tuple(a), tuple(b)) for a, b in ref], f"head {h}"
+    # merged rows: column picks <= qb, slash picks {qb-ob-1, qb-ob} clipped, diagonal (ref filtering.py:198-230)
+    i_c, i_s = sels[0].chunks[0].i_c, sels[0].chunks[0].i_s
+    for qb in (0, 1, 4095, 8191):
+        want = {kb for kb in i_c if kb <= qb} | {qb}
+        for ob in i_s:
+            want |= {kb for kb in (qb - ob - 1, qb - ob) if 0 <= kb <= qb}
+        assert tuple(int(x) for x in res.mask.head(0).active_for(qb)) == tuple(sorted(want)), qb
