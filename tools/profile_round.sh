@@ -17,6 +17,7 @@ timeout 300 python bench.py --config c2 --no-cpu > $OUT/bench_c2.json 2>> $OUT/b
 timeout 600 python bench.py --config c4 --no-cpu --no-e2e > $OUT/bench_c4_r2.json 2>> $OUT/bench.err
 timeout 600 python bench.py --config c4 --chunk-n 77 --no-dense --no-cpu --no-e2e > $OUT/bench_c4_r10.json 2>> $OUT/bench.err
 timeout 900 python bench.py --config c5 --steps 3 --no-dense --no-cpu --no-e2e > $OUT/bench_c5_1gpu.json 2>> $OUT/bench.err
+timeout 600 python bench.py --impl reference > $OUT/bench_reference.json 2>> $OUT/bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   timeout 300 python bench.py --steps 2 --warmup 3 --no-dense --no-cpu --no-e2e --no-graph > $OUT/ncu_launch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k3_share|k1_tc|k2_select|k2_merge|xf_pass|s1_fold" -s 0 -c 12 \
