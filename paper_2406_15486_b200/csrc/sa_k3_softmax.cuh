@@ -70,7 +70,12 @@ struct K3Prof {
 #define SA_K3_POLY 1
 #endif
 // SA_K3_EXP (timing experiments only): 1 = no softmax math (arrive at once),
-// 2 = no exponentials (P = the scaled score, finite garbage).
+// 2 = no exponentials (P = the scaled score, finite garbage), 3 = no math but
+// SA_K3_SPIN cycles of delay (separates the softmax's latency from its
+// resource use).
+#ifndef SA_K3_SPIN
+#define SA_K3_SPIN 1300
+#endif
 #ifndef SA_K3_EXP
 #define SA_K3_EXP 0
 #endif
@@ -221,7 +226,12 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
       }
     }
 #endif
-    if (SA_K3_EXP == 1) {
+    if (SA_K3_EXP == 1 || SA_K3_EXP == 3) {
+      if (SA_K3_EXP == 3) {  // timing experiment: a softmax that only takes SA_K3_SPIN cycles
+        const long long t0 = clock64();
+        while (clock64() - t0 < SA_K3_SPIN) {
+        }
+      }
       tc_fence_before();
       arrive_part();
       arrive_full();
@@ -380,6 +390,202 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
   }
   if (valid && lse) lse[(size_t)T.h * S + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
   if (i == 0 && touched) atomicAdd(reinterpret_cast<unsigned long long*>(touched + T.h), (unsigned long long)T.n);
+}
+
+// ---------------------------------------------------------------------------
+// Split-column softmax: EIGHT warps per tile, two per TMEM lane quadrant.
+// Warp (quad, half) owns rows quad*32..+31 and keys half*64..+63, so the
+// per-tile softmax latency -- which sits on the S -> softmax -> PV -> S chain
+// of every item -- is about half that of one warp per row.
+//   * Fast path (off-diagonal blocks after the first): one read of the warp's
+//     64 scores, exponentials against the running max m_ref, packed P held in
+//     registers.  The two halves of a row then meet at a named barrier
+//     (64 threads) to learn whether either saw a score above m_ref + 8; if
+//     not, P is stored and m_ref stays (the common case: no max exchange).
+//   * Otherwise (first block, diagonal block, max growth) both halves re-read
+//     their scores (still intact: P was not stored), exchange the half-row
+//     maxima through shared memory, rescale their 64 columns of O and their
+//     partial row sums, and store P.
+// Half h writes its bf16 P over the start of its own score columns (keys
+// 0..63 -> cols 0..31, keys 64..127 -> cols 64..95) and signals its own
+// p barrier (4 warps x 32 threads).  Row sums are combined in the epilogue.
+struct K3SplitBars {
+  uint64_t* s_full;   // S(j) landed in TMEM                 (tcgen05.commit)
+  uint64_t* p_half0;  // P(j) keys 0..63 in cols 0..31        (128 arrivals)
+  uint64_t* p_half1;  // P(j) keys 64..127 in cols 64..95     (128 arrivals)
+  uint64_t* o_full;   // last PV done                         (tcgen05.commit)
+};
+
+// xchg: float[3][2][128] per tile: [parity 0/1 | epilogue][half][row]; flags: int[2][2][4] per tile
+__device__ __forceinline__ void k3_softmax_split(const K3Tile& T, const K3SplitBars& b, uint32_t tS0, uint32_t tO0,
+                                                 int quad, int half, float* xchg, int* flags, int bar_id, int S,
+                                                 __nv_bfloat16* out, float* lse, long long* touched) {
+  const int i = quad * 32 + lane_id();  // query row within the tile
+  const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+  const uint32_t tS = tS0 + lane_off, tO = tO0 + lane_off;
+  const int c0 = half * 64;  // first key (= score column) of this warp
+  const float sl2 = 1.4426950408889634f * 0.08838834764831845f;  // log2(e) / sqrt(128)
+  const uint64_t sl2x2 = f32x2(sl2, sl2);
+  float m_ref = -INFINITY;
+  uint64_t lacc0 = f32x2(0.f, 0.f), lacc1 = f32x2(0.f, 0.f);
+  uint64_t* p_mine = half ? b.p_half1 : b.p_half0;
+  for (int j = 0; j < T.n; ++j) {
+    const int kb = __ldg(T.list + j);
+    const bool diag = kb == T.qb;  // warp-uniform
+    k3_wait(b.s_full, j & 1);
+    tc_fence_after();
+    uint32_t pk[32];
+    bool ok = false;
+    if (j > 0 && !diag) {  // fast path
+      const uint64_t negm = f32x2(-m_ref, -m_ref);
+      uint64_t bacc0 = f32x2(0.f, 0.f), bacc1 = f32x2(0.f, 0.f);
+      float ymax = -INFINITY;
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t r[32];
+        tmem_ld32_sync(tS + c0 + ch * 32, r);
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          float y0, y1;
+          unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm), y0, y1);
+          ymax = fmax3(ymax, y0, y1);
+          const uint64_t pp = ((t & 3) >= 4 - SA_K3_POLY) ? ex2_poly2(y0, y1) : f32x2(ex2(y0), ex2(y1));
+          if (t & 1)
+            bacc1 = fadd2(bacc1, pp);
+          else
+            bacc0 = fadd2(bacc0, pp);
+          float p0, p1;
+          unpack_f32x2(pp, p0, p1);
+          pk[ch * 16 + t] = pack_bf16(p0, p1);
+        }
+      }
+      const int bad = __any_sync(0xffffffffu, ymax > kK3RescaleThreshold);
+      int* fl = flags + (j & 1) * 8;  // parity double-buffered: [half][quad]
+      if (lane_id() == 0) fl[half * 4 + quad] = bad;
+      named_bar_sync(bar_id, 64);
+      ok = !(bad | fl[(half ^ 1) * 4 + quad]);
+      if (ok) {
+        lacc0 = fadd2(lacc0, bacc0);
+        lacc1 = fadd2(lacc1, bacc1);
+      }
+    }
+    if (!ok) {  // exact path: block max over the whole row (both halves), rescale, exponentials
+      float ma = -INFINITY, mb = -INFINITY;
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t r[32];
+        tmem_ld32_sync(tS + c0 + ch * 32, r);
+        if (diag) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (c0 + ch * 32 + t > i) r[t] = __float_as_uint(-INFINITY);
+        }
+#pragma unroll
+        for (int t = 0; t < 32; t += 4) {
+          ma = fmax3(ma, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
+          mb = fmax3(mb, __uint_as_float(r[t + 2]), __uint_as_float(r[t + 3]));
+        }
+      }
+      float mxs = fmaxf(ma, mb) * sl2;
+      {
+        float* slot = xchg + (j & 1) * 256;
+        slot[half * 128 + i] = mxs;
+        named_bar_sync(bar_id, 64);
+        mxs = fmaxf(mxs, slot[(half ^ 1) * 128 + i]);
+      }
+      // both halves hold the same row maxima: identical (warp-wide) decisions
+      if (__any_sync(0xffffffffu, mxs > m_ref + kK3RescaleThreshold)) {
+        const float m_new = fmaxf(m_ref, mxs);
+        if (j > 0) {
+          const float f = ex2(m_ref - m_new);
+          const uint64_t f2 = f32x2(f, f);
+          lacc0 = fmul2(lacc0, f2);
+          lacc1 = fmul2(lacc1, f2);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t o[16];
+            tmem_ld16_sync(tO + c0 + ch * 16, o);
+#pragma unroll
+            for (int t = 0; t < 16; t += 2) {
+              float a, c;
+              unpack_f32x2(fmul2(f32x2(__uint_as_float(o[t]), __uint_as_float(o[t + 1])), f2), a, c);
+              o[t] = __float_as_uint(a);
+              o[t + 1] = __float_as_uint(c);
+            }
+            tmem_st16(tO + c0 + ch * 16, o);
+          }
+        }
+        m_ref = m_new;
+      }
+      const uint64_t negm = f32x2(-m_ref, -m_ref);
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t r[32];
+        tmem_ld32_sync(tS + c0 + ch * 32, r);
+        if (diag) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (c0 + ch * 32 + t > i) r[t] = __float_as_uint(-INFINITY);
+        }
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          float y0, y1;
+          unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm), y0, y1);
+          const float p0 = ex2(y0), p1 = ex2(y1);
+          if (t & 1)
+            lacc1 = fadd2(lacc1, f32x2(p0, p1));
+          else
+            lacc0 = fadd2(lacc0, f32x2(p0, p1));
+          pk[ch * 16 + t] = pack_bf16(p0, p1);
+        }
+      }
+    }
+#pragma unroll
+    for (int ch = 0; ch < 2; ++ch) {
+      uint32_t(&q)[16] = *reinterpret_cast<uint32_t(*)[16]>(&pk[ch * 16]);
+      tmem_st16(tS + c0 + ch * 16, q);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    mbar_arrive(p_mine);
+  }
+  // ---- epilogue: combine the half-row sums, O / l -> bf16 (this warp's 64 columns)
+  float l;
+  {
+    float a0, a1, b0, b1;
+    unpack_f32x2(lacc0, a0, a1);
+    unpack_f32x2(lacc1, b0, b1);
+    l = (a0 + a1) + (b0 + b1);
+    float* slot = xchg + 2 * 256;
+    slot[half * 128 + i] = l;
+    named_bar_sync(bar_id, 64);
+    l += slot[(half ^ 1) * 128 + i];
+  }
+  k3_wait(b.o_full, 0);
+  tc_fence_after();
+  const int row = T.qb * 128 + i;
+  const bool valid = row < S;
+  const float inv = 1.f / l;
+  __nv_bfloat16* dst = out + ((size_t)T.h * S + row) * 128 + c0;
+  const uint64_t stream_out = policy_evict_first();
+#pragma unroll
+  for (int ch = 0; ch < 2; ++ch) {
+    uint32_t r[32];
+    tmem_ld32_sync(tO + c0 + ch * 32, r);
+    uint32_t o[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) o[t] = pack_bf16(__uint_as_float(r[2 * t]) * inv, __uint_as_float(r[2 * t + 1]) * inv);
+    if (valid) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst + ch * 32);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        st_global_v4_hint(d4 + t, make_uint4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]), stream_out);
+    }
+  }
+  if (half == 0) {
+    if (valid && lse) lse[(size_t)T.h * S + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
+    if (i == 0 && touched) atomicAdd(reinterpret_cast<unsigned long long*>(touched + T.h), (unsigned long long)T.n);
+  }
 }
 
 }  // namespace sa

@@ -33,8 +33,13 @@ namespace sa {
 namespace {
 
 // warp 0 TMA, warp 1 MMA, warps 2-3 idle (so each softmax warpgroup starts at
-// TMEM lane quadrant 0), warps 4-7 softmax of A, 8-11 softmax of B.
-constexpr int kWarps = 12;
+// TMEM lane quadrant 0), then the softmax warps: 4-7 for A and 8-11 for B, or
+// with SA_K3_SPLIT two warps per lane quadrant: 4-11 for A, 12-19 for B
+// (k3_softmax_split; more than 16 warps caps ptxas at 96 registers).
+#ifndef SA_K3_SPLIT
+#define SA_K3_SPLIT 0
+#endif
+constexpr int kWarps = SA_K3_SPLIT ? 20 : 12;
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kTileBytes = 128 * 128 * 2;
 constexpr uint32_t kBoxBytes = kTileBytes / 2;
@@ -43,8 +48,12 @@ constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 128, true);
 
 struct __align__(8) ShareSmem {
   uint64_t q_full[2], k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full[2], p_part[2], p_full[2], o_full[2];
+  uint64_t s_full[2], p_part[2], p_full[2], o_full[2];  // split softmax: p_part/p_full = keys 0..63 / 64..127
   uint32_t tmem_base;
+#if SA_K3_SPLIT
+  float xchg[2][768];  // per tile: half-row maxima [parity][half][row] and the epilogue row sums
+  int flags[2][16];    // per tile: max-growth votes [parity][half][quad]
+#endif
 };
 
 struct ShareParams {
@@ -206,15 +215,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int j = n_pv[x];
       const int s = step & 1;
       pf.start();
-      k3_wait(&sm->p_part[x], j & 1);
+      k3_wait(&sm->p_part[x], j & 1);  // (split softmax: keys 0..63)
       pf.stop(5);
       pf.start();
       k3_wait(&sm->v_full[s], (step >> 1) & 1);
       pf.stop(7);
       tc_fence_after();
       if (elect_one()) {
+        constexpr int kFirst = SA_K3_SPLIT ? 4 : 6;  // K-steps covered by the first P signal
 #pragma unroll
-        for (int kk = 0; kk < 6; ++kk)
+        for (int kk = 0; kk < kFirst; ++kk)
           umma_ts(tO[x], tS[x] + kk * 8, sdesc_sw128(v_addr0 + s * kTileBytes + kk * 2048, kBoxBytes, 1024), kIdescPV,
                   (j > 0 || kk > 0) ? 1u : 0u);
       }
@@ -224,10 +234,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       pf.stop(6);
       tc_fence_after();
       if (elect_one()) {
+        constexpr int kFirst = SA_K3_SPLIT ? 4 : 6;
+        constexpr uint32_t kSecondCol = SA_K3_SPLIT ? 32 : 0;  // split: P of keys 64..127 sits at cols 64..95
 #pragma unroll
-        for (int kk = 6; kk < 8; ++kk)
-          umma_ts(tO[x], tS[x] + kk * 8, sdesc_sw128(v_addr0 + s * kTileBytes + kk * 2048, kBoxBytes, 1024),
-                  kIdescPV, 1u);
+        for (int kk = kFirst; kk < 8; ++kk)
+          umma_ts(tO[x], tS[x] + kSecondCol + kk * 8,
+                  sdesc_sw128(v_addr0 + s * kTileBytes + kk * 2048, kBoxBytes, 1024), kIdescPV, 1u);
         if (j == T[x].n - 1) umma_commit(&sm->o_full[x]);
       }
       __syncwarp();
@@ -279,12 +291,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     pf.flush(lane_id() == 0);
   } else if (warp >= 4) {
+#if SA_K3_SPLIT
+    const int x = warp < 12 ? 0 : 1;
+    const int half = (warp >> 2) & 1;  // warps 4-7 / 12-15: keys 0..63; 8-11 / 16-19: keys 64..127
+    const int quad = warp & 3;
+    const K3Tile Tx = x ? T[1] : T[0];
+    if (Tx.n > 0) {
+      const K3SplitBars b{&sm->s_full[x], &sm->p_part[x], &sm->p_full[x], &sm->o_full[x]};
+      k3_softmax_split(Tx, b, x ? tS[1] : tS[0], x ? tO[1] : tO[0], quad, half, sm->xchg[x], sm->flags[x],
+                       1 + x * 4 + quad, P.S, P.out, P.lse, P.touched);
+    }
+#else
     const int x = warp < 8 ? 0 : 1;
     const K3Tile Tx = x ? T[1] : T[0];  // select, not a dynamically indexed (local-memory) array
     if (Tx.n > 0) {
       const K3TileBars b{&sm->s_full[x], &sm->p_part[x], &sm->p_full[x], &sm->o_full[x]};
       k3_softmax_tile<false>(Tx, b, x ? tS[1] : tS[0], x ? tO[1] : tO[0], warp & 3, P.S, P.out, P.lse, P.touched);
     }
+#endif
   }
   tc_fence_before();
   __syncthreads();
