@@ -33,6 +33,37 @@ def _as_host(x) -> torch.Tensor:
     return x.contiguous()
 
 
+def _group_plan(Hq: int, group: int, hpg: int) -> list:
+    """Head groups [h0, h1) inside KV-group boundaries.  The first groups of
+    the batch are small (1, then 2 heads) so the first kernels start after a
+    short copy, and the last groups shrink again (2, then 1) so the final
+    device->host copy after the last kernel is short; the rest use `hpg`."""
+    sizes_per_kv = []
+    n_kv = Hq // group
+    for g in range(n_kv):
+        head, tail = [], []
+        rest = group
+        if g == 0:
+            for s in (1, 2):
+                if rest > s:
+                    head.append(s)
+                    rest -= s
+        if g == n_kv - 1:
+            for s in (1, 2):
+                if rest > s:
+                    tail.insert(0, s)
+                    rest -= s
+        n_mid = -(-rest // hpg)  # near-equal middle groups of at most hpg heads
+        mid = [rest // n_mid + (1 if i < rest % n_mid else 0) for i in range(n_mid)] if rest else []
+        sizes_per_kv.append(head + mid + tail)
+    groups, h0 = [], 0
+    for sizes in sizes_per_kv:
+        for s in sizes:
+            groups.append((h0, h0 + s))
+            h0 += s
+    return groups
+
+
 def sample_attention_host(q, k, v, heads_per_group: int = 4, device=None, out: torch.Tensor | None = None,
                           check_inputs: bool = True, dtype=torch.bfloat16, **kw):
     """q [Hq,S,d], k/v [Hkv,S,d] on the host -> (out [Hq,S,d] on the host,
@@ -66,7 +97,7 @@ def sample_attention_host(q, k, v, heads_per_group: int = 4, device=None, out: t
     h2d = torch.cuda.Stream(device=dev)
     d2h = torch.cuda.Stream(device=dev)
     h2d.wait_stream(compute)  # dq/dk/dv were allocated on the compute stream
-    groups = [(h0, h0 + hpg) for h0 in range(0, Hq, hpg)]
+    groups = _group_plan(Hq, group, hpg)
     ready = []
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     with torch.cuda.stream(h2d):
