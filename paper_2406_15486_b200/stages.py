@@ -45,12 +45,24 @@ GUARD_EPS = 4e-7
 _WS_CACHE: dict = {}
 
 
+_WS_PRIVATE: dict = {}
+
+
+def _ws_key(b: HeadBatch, blk: int, cn: int, stream: bool = True):
+    # per stream: calls on different streams may run concurrently
+    geom = (b.q.device, b.S, b.Hq, b.Hkv, b.d, blk, cn, b.dtype_code)
+    return geom + (b.stream,) if stream else geom
+
+
 def _workspace(b: HeadBatch, blk: int, cn: int) -> torch.Tensor:
-    key = (b.q.device, b.S, b.Hq, b.Hkv, b.d, blk, cn, b.dtype_code)
+    ws = _WS_PRIVATE.get(_ws_key(b, blk, cn, stream=False))
+    if ws is not None:
+        return ws
+    key = _ws_key(b, blk, cn)
     ws = _WS_CACHE.get(key)
     if ws is None:
         nbytes = int(_lib.load().sa_workspace_bytes(b.S, b.Hq, b.Hkv, b.d, blk, cn, b.dtype_code))
-        if len(_WS_CACHE) > 8:
+        if len(_WS_CACHE) > 16:
             _WS_CACHE.clear()
         ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=b.q.device)
         _WS_CACHE[key] = ws
@@ -59,18 +71,21 @@ def _workspace(b: HeadBatch, blk: int, cn: int) -> torch.Tensor:
 
 @contextlib.contextmanager
 def private_workspace(b: HeadBatch, blk: int, cn: int):
-    """Within the block, stage calls on this geometry use a fresh workspace
-    that is NOT shared with later calls (CUDA-graph capture: the graph keeps
-    the pointer, so it must own the buffer).  Yields the workspace tensor."""
-    key = (b.q.device, b.S, b.Hq, b.Hkv, b.d, blk, cn, b.dtype_code)
-    saved = _WS_CACHE.pop(key, None)
-    ws = _workspace(b, blk, cn)
+    """Within the block, stage calls on this geometry (on any stream) use a
+    fresh workspace that is NOT shared with later calls (CUDA-graph capture:
+    the graph keeps the pointer, so it must own the buffer).  Yields it."""
+    geom = _ws_key(b, blk, cn, stream=False)
+    nbytes = int(_lib.load().sa_workspace_bytes(b.S, b.Hq, b.Hkv, b.d, blk, cn, b.dtype_code))
+    ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=b.q.device)
+    saved = _WS_PRIVATE.get(geom)
+    _WS_PRIVATE[geom] = ws
     try:
         yield ws
     finally:
-        _WS_CACHE.pop(key, None)
-        if saved is not None:
-            _WS_CACHE[key] = saved
+        if saved is None:
+            _WS_PRIVATE.pop(geom, None)
+        else:
+            _WS_PRIVATE[geom] = saved
 
 
 def as_batch(heads, dtype=None) -> HeadBatch:
