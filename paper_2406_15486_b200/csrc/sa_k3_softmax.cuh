@@ -72,12 +72,16 @@ struct K3Prof {
 // SA_K3_EXP (timing experiments only): 1 = no softmax math (arrive at once),
 // 2 = no exponentials (P = the scaled score, finite garbage), 3 = no math but
 // SA_K3_SPIN cycles of delay (separates the softmax's latency from its
-// resource use).
+// resource use), 4 = the softmax's TMEM reads and writes without the math.
 #ifndef SA_K3_SPIN
 #define SA_K3_SPIN 1300
 #endif
 #ifndef SA_K3_EXP
 #define SA_K3_EXP 0
+#endif
+// Fast path exponentials as ex2.approx.f16x2 (one MUFU op per pair; experiment).
+#ifndef SA_K3_EXPH
+#define SA_K3_EXPH 0
 #endif
 // Single-read fast path for off-diagonal blocks (see k3_softmax_tile).
 #ifndef SA_K3_FAST
@@ -193,7 +197,9 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
             unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm),
                          y0, y1);
             ymax = fmax3(ymax, y0, y1);
-            const uint64_t pp = ((t & 3) >= 4 - SA_K3_POLY) ? ex2_poly2(y0, y1) : f32x2(ex2(y0), ex2(y1));
+            const uint64_t pp = SA_K3_EXPH ? ex2_h2(y0, y1)
+                                : ((t & 3) >= 4 - SA_K3_POLY) ? ex2_poly2(y0, y1)
+                                                              : f32x2(ex2(y0), ex2(y1));
             if (t & 1)
               bacc1 = fadd2(bacc1, pp);
             else
@@ -226,6 +232,26 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
       }
     }
 #endif
+    if (SA_K3_EXP == 4) {  // timing experiment: the softmax's TMEM traffic only (read S, write P), no math
+      uint32_t acc = 0;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[32];
+        tmem_ld32_sync(tS + ch * 32, r);
+#pragma unroll
+        for (int t = 0; t < 32; ++t) acc ^= r[t];
+      }
+      uint32_t pk[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) pk[t] = acc & 0x3c003c00u;  // small finite bf16 pairs
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) tmem_st16(tS + ch * 16, pk);
+      tmem_st_wait();
+      tc_fence_before();
+      arrive_part();
+      arrive_full();
+      continue;
+    }
     if (SA_K3_EXP == 1 || SA_K3_EXP == 3) {
       if (SA_K3_EXP == 3) {  // timing experiment: a softmax that only takes SA_K3_SPIN cycles
         const long long t0 = clock64();

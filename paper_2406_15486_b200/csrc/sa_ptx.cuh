@@ -434,6 +434,20 @@ __device__ __forceinline__ uint64_t ex2_poly2(float x0, float x1) {
   return r;
 }
 
+// 2^x for a pair on ONE MUFU op: f32x2 -> f16x2, ex2.approx.f16x2, back to
+// f32x2 (a probability that is rounded to bf16 for the PV MMA anyway; inputs
+// below -24 flush to 0).
+__device__ __forceinline__ uint64_t ex2_h2(float x0, float x1) {
+  uint32_t h, e;
+  asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(x0), "f"(x1));
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
+  float y0, y1;
+  asm("{\n\t.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
+      : "=f"(y0), "=f"(y1)
+      : "r"(e));
+  return f32x2(y0, y1);
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
