@@ -197,8 +197,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       pf.flush(true);
     }
   } else if (warp == 1) {
-    const uint32_t q_addr[2] = {smem_u32(sQ[0]), smem_u32(sQ[1])};
-    const uint32_t k_addr0 = smem_u32(sK0), v_addr0 = smem_u32(sV0);
+    // Descriptors are linear in the smem address (start address >> 4 in the low
+    // bits), so each operand is a precomputed base plus a constant: keeps the
+    // issuer's per-MMA work to one add on a sub-partition shared with softmax warps.
+    const uint64_t q_desc[2] = {sdesc_sw128(smem_u32(sQ[0]), 16, 1024), sdesc_sw128(smem_u32(sQ[1]), 16, 1024)};
+    const uint64_t k_desc0 = sdesc_sw128(smem_u32(sK0), 16, 1024);
+    const uint64_t v_desc0 = sdesc_sw128(smem_u32(sV0), kBoxBytes, 1024);
     int n_s[2] = {0, 0};      // S MMAs issued per item
     int n_pv[2] = {0, 0};     // PV MMAs issued per item
     int pend[2] = {-1, -1};   // union step whose PV is still to be issued
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int kFirst = SA_K3_SPLIT ? 4 : 6;  // K-steps covered by the first P signal
 #pragma unroll
         for (int kk = 0; kk < kFirst; ++kk)
-          umma_ts(tO[x], tS[x] + kk * 8, sdesc_sw128(v_addr0 + s * kTileBytes + kk * 2048, kBoxBytes, 1024), kIdescPV,
+          umma_ts(tO[x], tS[x] + kk * 8, v_desc0 + ((s * kTileBytes + kk * 2048) >> 4), kIdescPV,
                   (j > 0 || kk > 0) ? 1u : 0u);
       }
       __syncwarp();
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = kFirst; kk < 8; ++kk)
           umma_ts(tO[x], tS[x] + kSecondCol + kk * 8,
-                  sdesc_sw128(v_addr0 + s * kTileBytes + kk * 2048, kBoxBytes, 1024), kIdescPV, 1u);
+                  v_desc0 + ((s * kTileBytes + kk * 2048) >> 4), kIdescPV, 1u);
         if (j == T[x].n - 1) umma_commit(&sm->o_full[x]);
       }
       __syncwarp();
@@ -265,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               const uint32_t off = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
-              umma_ss(tS[x], sdesc_sw128(q_addr[x] + off, 16, 1024), sdesc_sw128(k_addr0 + s * kTileBytes + off, 16, 1024),
+              umma_ss(tS[x], q_desc[x] + (off >> 4), k_desc0 + ((s * kTileBytes + off) >> 4),
                       kIdescQK, kk > 0 ? 1u : 0u);
             }
             umma_commit(&sm->s_full[x]);
