@@ -375,6 +375,21 @@ def main():
              "block_density": round(flop.block_density, 4),
              "rescored_pairs": res.n_rescored(),
              "kept_tflop": round(kept / 1e12, 3), "dense_tflop": round(dense_job / world / 1e12, 3)}
+    # stages 1 and 2 are bandwidth / latency bound: algorithmic HBM bytes over the stage time
+    hq_loc, hkv_loc = q.shape[0], k.shape[0]
+    nb = -(-S // 128)
+    pairs = hq_loc * chunk_n
+    s1_bytes = (hkv_loc * S * d * 2 + pairs * 128 * d * 2      # K once per KV head, sampled Q rows
+                + 2 * 3 * 4 * pairs * 128 * nb                 # (A, B, m) partials written, then read by the fold
+                + 2 * 8 * pairs * nb)                          # col / slash out
+    s2_bytes = (2 * 8 * pairs * nb + 2 * 4 * pairs * nb        # scores in, picks out
+                + 4 * sum(f.active_blocks for f in flops) + 4 * hq_loc * nb)  # merged lists + counts
+    t1_ms, t2_ms = extra["stage_ms"]["stage1"], extra["stage_ms"]["stage2"]
+    extra["stage_bandwidth"] = {
+        "stage1": {"algorithmic_bytes": s1_bytes, "GB/s": round(s1_bytes / (t1_ms * 1e6), 1) if t1_ms else None},
+        "stage2": {"algorithmic_bytes": s2_bytes, "GB/s": round(s2_bytes / (t2_ms * 1e6), 1) if t2_ms else None,
+                   "note": "includes the fp64 re-score of the guard-flagged pairs"},
+        "hbm_peak_GB/s": pk.get("hbm_gbs")}
 
     # ---- dense comparison rows (same GPU, same inputs)
     if not args.no_dense and rank == 0:

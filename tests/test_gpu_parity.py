@@ -317,3 +317,25 @@ def test_head_shards_match_full_batch(sa, Hq, Hkv, world):
         assert torch.equal(o, full[s.q_heads[0]: s.q_heads[-1] + 1])
         assert torch.equal(og, o)
         assert torch.equal(rs.mask.kv_cnt, res.mask.kv_cnt[s.q_heads[0]: s.q_heads[-1] + 1])
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,cn", [(100, 2, 1, 1), (129, 3, 1, 2), (777, 5, 1, 3)])
+def test_short_and_mqa_sequences(sa, S, Hq, Hkv, cn):
+    """bf16 tensor-core path on S < 128 (one window [0, S), ref sampler.py:99-101),
+    S = 129 (a one-key trailing block), ragged S, MQA (one KV head for all q
+    heads) and odd head counts (the unit schedule pairs adjacent query blocks)."""
+    rng = np.random.default_rng(S)
+    qs = [O_bf16(rng.standard_normal((S, 128)) * 1.5) for _ in range(Hq)]
+    ks = [O_bf16(rng.standard_normal((S, 128)) * 1.5) for _ in range(Hkv)]
+    vs = [O_bf16(rng.standard_normal((S, 128))) for _ in range(Hkv)]
+    qt = torch.from_numpy(np.stack(qs)).to("cuda", torch.bfloat16)
+    kt = torch.from_numpy(np.stack(ks)).to("cuda", torch.bfloat16)
+    vt = torch.from_numpy(np.stack(vs)).to("cuda", torch.bfloat16)
+    out, res = sa.sample_attention(qt, kt, vt, alpha=0.9, chunk_n=cn)
+    sels = res.mask.selections()
+    g = Hq // Hkv
+    for h in range(Hq):
+        r = O.run_head(qs[h], ks[h // g], vs[h // g], 0.9, 0.9, cn, 128)
+        assert [(c.i_c, c.i_s) for c in sels[h].chunks] == r["selection"], h
+        assert np.array_equal(res.mask.to_dense()[h], r["grid"]), h
+        assert np.abs(out[h].float().cpu().numpy() - r["out"]).max() <= BF16_TOL, h
