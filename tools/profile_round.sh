@@ -20,6 +20,6 @@ timeout 900 python bench.py --config c5 --steps 3 --no-dense --no-cpu --no-e2e >
 timeout 600 python bench.py --impl reference > $OUT/bench_reference.json 2>> $OUT/bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   timeout 300 python bench.py --steps 2 --warmup 3 --no-dense --no-cpu --no-e2e --no-graph > $OUT/ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k3_share|k1_tc|k2_select|k2_merge|xf_pass|s1_fold" -s 0 -c 12 \
+ncu --set full --clock-control none --import-source on -k regex:"k3_share|k1_tc|k2_|xf_pass|s1_|k_check|k_flag" -s 0 -c 20 \
   -o $OUT/full timeout 600 python bench.py --steps 1 --warmup 3 --no-dense --no-cpu --no-e2e --no-graph > $OUT/ncu_full.log 2>&1
 ls -la $OUT
