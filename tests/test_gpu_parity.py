@@ -339,3 +339,27 @@ def test_short_and_mqa_sequences(sa, S, Hq, Hkv, cn):
         assert [(c.i_c, c.i_s) for c in sels[h].chunks] == r["selection"], h
         assert np.array_equal(res.mask.to_dense()[h], r["grid"]), h
         assert np.abs(out[h].float().cpu().numpy() - r["out"]).max() <= BF16_TOL, h
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_lse_matches_masked_logsumexp(sa, dtype):
+    """return_lse: per row log(sum over the mask's active causal keys of
+    exp(q.k/sqrt(d))), against an fp64 torch computation on the same mask."""
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    S, Hq, Hkv = 1000, 2, 1
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q = (torch.randn((Hq, S, 128), generator=g, device="cuda") * 1.2).to(tdt)
+    k = (torch.randn((Hkv, S, 128), generator=g, device="cuda") * 1.2).to(tdt)
+    v = torch.randn((Hkv, S, 128), generator=g, device="cuda").to(tdt)
+    out, res = sa.sample_attention(q, k, v, alpha=0.9, chunk_n=2, return_lse=True)
+    grids = torch.from_numpy(res.mask.to_dense()).cuda()  # [H, nb, nb]
+    nb = grids.shape[1]
+    rows = torch.arange(S, device="cuda")
+    for h in range(Hq):
+        s = (q[h].double() @ k[0].double().T) / np.sqrt(128)
+        keep = grids[h][rows // 128][:, rows // 128] & (rows[None, :] <= rows[:, None])
+        s = torch.where(keep, s, torch.tensor(float("-inf"), device="cuda", dtype=torch.float64))
+        ref = torch.logsumexp(s, dim=1)
+        err = (res.lse[h].double() - ref).abs().max().item()
+        assert err <= (2e-3 if dtype == "bf16" else 1e-5), (h, err)  # fp32 math: ~1e-7 relative on |lse| ~ 10
+    assert nb == 8
