@@ -30,6 +30,7 @@ SOURCES = [
     "sa_sparse_tc.cu",
     "sa_sparse_share.cu",
     "sa_sparse_pair.cu",
+    "sa_sparse_half.cu",
     "sa_sparse_simt.cu",
 ]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -219,8 +219,11 @@ int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, in
       const char* e = getenv("SA_K3_IMPL");
       if (e && e[0] == 's') return 1;  // "single": one item per CTA, two CTAs per SM (no K/V sharing)
       if (e && e[0] == 'p') return 2;  // "pair": units over SM pairs (cta_group::2)
+      if (e && e[0] == 'h') return 3;  // "half": units with half-block S buffers
       return 0;                        // "share": units in one CTA
     }();
+    if (impl == 3)
+      return launch_sparse_half(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse, touched, st);
     if (impl == 2)
       return launch_sparse_pair(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse, touched, st);
     if (impl == 1)
