@@ -77,3 +77,43 @@ def test_product_package_never_imports_oracle():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg, fn)).read()
             assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\S+)", src, re.M), fn
+
+
+def _err(lib):
+    return lib.sa_last_error().decode()
+
+
+def test_c_abi_rejects_bad_arguments_without_touching_the_gpu():
+    """Argument validation of the C ABI runs before any CUDA call (so it is
+    testable on a CPU host) and maps to the reference's exception classes."""
+    lib = _lib.load()
+    fake = 0x1000  # never dereferenced: every call below fails validation first
+    # stage 1: unsupported tensor-core shape (d != 128), bad plan layout, too small workspace
+    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 2, 1, 64, 128, 2, 0, 1, 4096, fake, fake,
+                       _lib.SA_STAGE1_TENSOR, None, fake, 1 << 30, None)
+    assert rc == _lib.SA_ERR_UNSUPPORTED and "d == 128" in _err(lib)
+    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 2, 1, 128, 128, 2, 0, 3, 4000, fake, fake,
+                       _lib.SA_STAGE1_TENSOR, None, fake, 1 << 30, None)
+    assert rc == _lib.SA_ERR_INVALID and "plan_chunks" in _err(lib)
+    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 2, 1, 128, 128, 2, 0, 1, 4096, fake, fake,
+                       _lib.SA_STAGE1_TENSOR, None, fake, 16, None)
+    assert rc == _lib.SA_ERR_INVALID and "workspace" in _err(lib)
+    # GQA mapping past the supplied kv heads
+    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 4, 1, 128, 128, 2, 0, 1, 4096, fake, fake,
+                       _lib.SA_STAGE1_TENSOR, None, fake, 1 << 30, None)
+    assert rc == _lib.SA_ERR_INVALID and "kv heads" in _err(lib)
+    # stage 2: alpha outside [0, 1] (ref sampler.py:52-56), guard without flags
+    assert lib.sa_select(fake, fake, 1, 1, 8, 1.5, 0.9, 0.0, None, None, None, fake, fake, None) == _lib.SA_ERR_INVALID
+    assert "alpha_c" in _err(lib)
+    assert lib.sa_select(fake, fake, 1, 1, 8, 0.9, 0.9, 1e-7, None, None, None, fake, fake, None) == _lib.SA_ERR_INVALID
+    assert lib.sa_merge(fake, fake, 1, 1, 7, 1024, 128, 1024, 0, 1, fake, fake, None, None, None) == _lib.SA_ERR_INVALID
+    assert lib.sa_schedule_len(0, 8, 1, 0) < 0
+    assert lib.sa_schedule_len(32, 1024, 16, 0) == 2 * 32 * 1024 // 2
+    assert lib.sa_schedule_len(3, 5, 3, 0) == 2 * (5 + 3)  # one head pair + the odd head's adjacent-block pairs
+    # stage 3: fp32 path limits
+    rc = lib.sa_sparse_forward(fake, fake, fake, _lib.SA_FP32, 512, 1, 1, 256, 128, 1, 0, fake, fake, None, fake,
+                               None, None, None)
+    assert rc == _lib.SA_ERR_UNSUPPORTED
+    # the Python wrapper turns these codes into the reference's exception types
+    with pytest.raises(sa.InputError):
+        _lib.call("sa_schedule", None, 1, 1, 1, 0, None, None)
