@@ -30,7 +30,13 @@ struct K3TileBars {
   uint64_t* o_full;  // last PV done                   (tcgen05.commit)
 };
 
-constexpr float kK3RescaleThreshold = 8.0f;  // log2 units
+// Lazy rescale: O is rescaled (and, on the single-read fast path, the block
+// redone) only when a row's max grows by more than this many log2 units, so
+// unnormalised P stays <= 2^threshold (bf16 / fp32 safe far beyond 2^16).
+#ifndef SA_K3_RESCALE_LOG2
+#define SA_K3_RESCALE_LOG2 8.0f
+#endif
+constexpr float kK3RescaleThreshold = SA_K3_RESCALE_LOG2;  // log2 units
 
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
