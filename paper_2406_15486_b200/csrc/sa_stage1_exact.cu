@@ -154,6 +154,115 @@ __device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __rest
 }
 
 
+#ifndef SA_XF_DMMA
+#define SA_XF_DMMA 1  // FP64 tensor-core inner products (0: the SIMT 8x8 register-tile version)
+#endif
+constexpr int kPitchD = 68;  // DMMA staging pitch (doubles): conflict-free fragment loads
+
+template <typename T>
+__device__ void stage_p(double* dst, const T* src, int n, int d, int c0) {
+  const int cn = min(kDChunk, d - c0);
+  for (int e = threadIdx.x; e < kRows * kDChunk; e += kThreads) {
+    const int r = e / kDChunk, c = e - r * kDChunk;
+    dst[r * kPitchD + c] = (r < n && c < cn) ? (double)to_f(src[(size_t)r * d + c0 + c]) : 0.0;
+  }
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// xf_work on the FP64 tensor cores (mma.sync m8n8k4): warp w owns rows
+// 16w..16w+15 (two 8-row tiles) x all 128 keys (sixteen 8-key tiles); lane
+// (g = lane / 4, c = lane % 4) holds rows 16w + 8mt + g, keys 8nt + 2c + {0, 1}.
+template <typename T>
+__device__ __forceinline__ void xf_work_dmma(const T* __restrict__ q, const T* __restrict__ k, const Stage1Geom& g,
+                                             int hc, int kb0, int kb1, double* __restrict__ pa,
+                                             double* __restrict__ pb, double* __restrict__ pm, double* qs,
+                                             double* ks) {
+  const int h = hc / g.cn, c = hc - h * g.cn;
+  const Win w = window_of(c, g.S, g.blk, g.itv);
+  kb1 = min(kb1, w.nkb);
+  const int kvh = kv_head_of(h, g.group, g.q_head0);
+  const int nr = w.se - w.ss, d = g.d, blk = g.blk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tg = lane & 3;
+  const T* qh = q + ((size_t)h * g.S + w.ss) * d;
+  const T* kh = k + (size_t)kvh * g.S * d;
+  const double scale = 1.0 / sqrt((double)d);
+  double m_run[2] = {-INFINITY, -INFINITY};
+  for (int kb = kb0; kb < kb1; ++kb) {
+    const int key0 = kb * blk;
+    const int nk = min(blk, w.se - key0);
+    double acc[2][16][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    for (int c0 = 0; c0 < d; c0 += kDChunk) {
+      __syncthreads();
+      stage_p(qs, qh, nr, d, c0);
+      stage_p(ks, kh + (size_t)key0 * d, nk, d, c0);
+      __syncthreads();
+      const int cn = min(kDChunk, d - c0);
+      for (int kc = 0; kc < cn; kc += 4) {
+        double a[2], b[16];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) a[mt] = qs[(16 * warp + 8 * mt + gq) * kPitchD + kc + tg];
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt) b[nt] = ks[(8 * nt + gq) * kPitchD + kc + tg];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 16; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int rl = 16 * warp + 8 * mt + gq;
+      const int row = w.ss + rl;
+      double mx = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int t = 8 * nt + 2 * tg + e;
+          acc[mt][nt][e] *= scale;
+          if (t < nk && key0 + t <= row) mx = fmax(mx, acc[mt][nt][e]);
+        }
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const double m_new = fmax(m_run[mt], mx);
+      const int rho = row % blk;
+      double sa_ = 0.0, sb_ = 0.0;
+      if (m_new != -INFINITY) {
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int t = 8 * nt + 2 * tg + e;
+            if (t < nk && key0 + t <= row) {
+              const double p = exp(acc[mt][nt][e] - m_new);
+              if (t <= rho) sa_ += p; else sb_ += p;
+            }
+          }
+      }
+      sa_ += __shfl_xor_sync(0xffffffffu, sa_, 1);
+      sb_ += __shfl_xor_sync(0xffffffffu, sb_, 1);
+      sa_ += __shfl_xor_sync(0xffffffffu, sa_, 2);
+      sb_ += __shfl_xor_sync(0xffffffffu, sb_, 2);
+      m_run[mt] = m_new;
+      if (tg == 0 && rl < nr) {
+        const size_t o = ((size_t)hc * blk + rl) * g.nb + kb;
+        pa[o] = sa_;
+        pb[o] = sb_;
+        pm[o] = m_new;
+      }
+    }
+  }
+}
+
 // One CTA per (key-block split, pair slot).  For the guard's re-score every
 // key block gets its own CTA so the few flagged pairs spread over all SMs, and
 // the pair slots loop over the compacted flagged list (L.flag_list).
@@ -162,13 +271,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     xf_pass(const T* __restrict__ q, const T* __restrict__ k, Stage1Geom g, const int* __restrict__ list,
             int kb_per_cta, double* __restrict__ pa, double* __restrict__ pb, double* __restrict__ pm) {
   extern __shared__ double smem_d[];
-  double* qs = smem_d;                          // [kRows][kDChunk+1]
-  double* ks = smem_d + kRows * (kDChunk + 1);  // [kKeys][kDChunk+1]
+  double* qs = smem_d;                                              // [kRows][pitch]
+  double* ks = smem_d + kRows * (SA_XF_DMMA ? kPitchD : kDChunk + 1);  // [kKeys][pitch]
   const int n_pairs = list ? list[0] : g.Hq * g.cn;
   const int kb0 = blockIdx.x * kb_per_cta;
   for (int f = blockIdx.y; f < n_pairs; f += gridDim.y) {  // uniform per CTA
     const int hc = list ? list[1 + f] : f;
+#if SA_XF_DMMA
+    xf_work_dmma(q, k, g, hc, kb0, kb0 + kb_per_cta, pa, pb, pm, qs, ks);
+#else
     xf_work(q, k, g, hc, kb0, kb0 + kb_per_cta, pa, pb, pm, qs, ks);
+#endif
     __syncthreads();  // qs / ks are reused by the next pair
   }
 }
@@ -338,7 +451,7 @@ namespace {
 template <typename T>
 int run_exact(const Stage1Geom& g, const T* q, const T* k, const int* only, char* ws, const Workspace& L,
               double* col, double* slash, cudaStream_t st) {
-  const size_t smem = (size_t)(kRows + kKeys) * (kDChunk + 1) * sizeof(double);
+  const size_t smem = (size_t)(kRows + kKeys) * (SA_XF_DMMA ? kPitchD : kDChunk + 1) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(xf_pass<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
