@@ -1,5 +1,8 @@
-"""Time the stage-3 kernel in dense mode under the SA_K3_EXP experiment
-variants (0 full, 1 no softmax math, 2 no MMA, 3 neither) in subprocesses."""
+"""Time the round-1 single-item stage-3 kernel (k3_tc, selected with
+SA_K3_IMPL=single) in dense mode under its runtime SA_K3_EXP variants
+(0 full, 1 no softmax math, 2 no MMA, 3 neither) in subprocesses.  The product
+kernel k3_share takes its experiment variants at build time instead
+(SA_NVCC_EXTRA=-DSA_K3_EXP=..., see tools/k3_variants.sh)."""
 import json, os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 CODE = r'''
@@ -23,7 +26,7 @@ libs = sys.argv[1:] or [""]
 modes = [int(m) for m in os.environ.get("MODES", "0,1,2,3").split(",")]
 for lib in libs:
     for mode in modes:
-        env = dict(os.environ, SA_K3_EXP=str(mode))
+        env = dict(os.environ, SA_K3_EXP=str(mode), SA_K3_IMPL="single")
         if lib:
             env["SA_LIB_PATH"] = os.path.abspath(lib)
         out = subprocess.run([sys.executable, "-c", CODE], env=env, capture_output=True, text=True)
