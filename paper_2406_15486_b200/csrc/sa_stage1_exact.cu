@@ -25,7 +25,16 @@
 namespace sa {
 namespace {
 
-constexpr int kThreads = 256;  // 16 x 16: ty -> rows ty + 16a (a < 8), tx -> keys tx + 16b (b < 8)
+#ifndef SA_XF_DMMA
+#define SA_XF_DMMA 1  // FP64 tensor-core inner products (0: the SIMT 8x8 register-tile version)
+#endif
+#ifndef SA_XF_W16
+#define SA_XF_W16 1  // DMMA with 16 warps of one 8-row tile each (0: 8 warps of two tiles)
+#endif
+// SIMT: 16 x 16 threads, ty -> rows ty + 16a (a < 8), tx -> keys tx + 16b (b < 8).
+// DMMA: warp w -> rows kMT*8*w .. +kMT*8 (kMT 8-row tiles) x all 128 keys.
+constexpr int kThreads = (SA_XF_DMMA && SA_XF_W16) ? 512 : 256;
+constexpr int kMT = (SA_XF_DMMA && SA_XF_W16) ? 1 : 2;
 constexpr int kRows = 128;
 constexpr int kKeys = 128;
 constexpr int kDChunk = 64;    // head-dim slice staged per round
@@ -154,9 +163,6 @@ __device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __rest
 }
 
 
-#ifndef SA_XF_DMMA
-#define SA_XF_DMMA 1  // FP64 tensor-core inner products (0: the SIMT 8x8 register-tile version)
-#endif
 constexpr int kPitchD = 68;  // DMMA staging pitch (doubles): conflict-free fragment loads
 
 template <typename T>
@@ -191,13 +197,15 @@ __device__ __forceinline__ void xf_work_dmma(const T* __restrict__ q, const T* _
   const T* qh = q + ((size_t)h * g.S + w.ss) * d;
   const T* kh = k + (size_t)kvh * g.S * d;
   const double scale = 1.0 / sqrt((double)d);
-  double m_run[2] = {-INFINITY, -INFINITY};
+  double m_run[kMT];
+#pragma unroll
+  for (int mt = 0; mt < kMT; ++mt) m_run[mt] = -INFINITY;
   for (int kb = kb0; kb < kb1; ++kb) {
     const int key0 = kb * blk;
     const int nk = min(blk, w.se - key0);
-    double acc[2][16][2];
+    double acc[kMT][16][2];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < kMT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 16; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
     for (int c0 = 0; c0 < d; c0 += kDChunk) {
@@ -207,20 +215,20 @@ __device__ __forceinline__ void xf_work_dmma(const T* __restrict__ q, const T* _
       __syncthreads();
       const int cn = min(kDChunk, d - c0);
       for (int kc = 0; kc < cn; kc += 4) {
-        double a[2], b[16];
+        double a[kMT], b[16];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) a[mt] = qs[(16 * warp + 8 * mt + gq) * kPitchD + kc + tg];
+        for (int mt = 0; mt < kMT; ++mt) a[mt] = qs[(8 * kMT * warp + 8 * mt + gq) * kPitchD + kc + tg];
 #pragma unroll
         for (int nt = 0; nt < 16; ++nt) b[nt] = ks[(8 * nt + gq) * kPitchD + kc + tg];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < kMT; ++mt)
 #pragma unroll
           for (int nt = 0; nt < 16; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
       }
     }
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const int rl = 16 * warp + 8 * mt + gq;
+    for (int mt = 0; mt < kMT; ++mt) {
+      const int rl = 8 * kMT * warp + 8 * mt + gq;
       const int row = w.ss + rl;
       double mx = -INFINITY;
 #pragma unroll
