@@ -154,16 +154,28 @@ __global__ void __launch_bounds__(kThreads, 2)
       tc_fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * 128;
       const int lim = row - kb * 128;  // keys t <= lim are causal
+      // every key of the block is causal for every row of the window: no per-element mask (warp-uniform)
+      const bool full = kb * 128 + 127 < ss;
       float mx = -INFINITY;
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32];
         tmem_ld32(taddr + ch * 32, r);
         tmem_ld_wait();
+        if (full) {
+          float mb = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float x = __uint_as_float(r[i]);
-          if (ch * 32 + i <= lim) mx = fmaxf(mx, x);
+          for (int i = 0; i < 32; i += 4) {
+            mx = fmax3(mx, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+            mb = fmax3(mb, __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+          }
+          mx = fmaxf(mx, mb);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float x = __uint_as_float(r[i]);
+            if (ch * 32 + i <= lim) mx = fmaxf(mx, x);
+          }
         }
       }
       const float m_new = fmaxf(m_run, mx * sl2);
@@ -175,11 +187,19 @@ __global__ void __launch_bounds__(kThreads, 2)
         uint32_t r[32];
         tmem_ld32(taddr + ch * 32, r);
         tmem_ld_wait();
+        if (full) {  // same values and summation order as the masked loop, minus the mask
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int t = ch * 32 + i;
-          const float p = t <= lim_e ? ex2(fmaf(__uint_as_float(r[i]), sl2, -m_new)) : 0.f;
-          if (t <= rho) a += p; else b += p;
+          for (int i = 0; i < 32; ++i) {
+            const float p = ex2(fmaf(__uint_as_float(r[i]), sl2, -m_new));
+            if (ch * 32 + i <= rho) a += p; else b += p;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int t = ch * 32 + i;
+            const float p = t <= lim_e ? ex2(fmaf(__uint_as_float(r[i]), sl2, -m_new)) : 0.f;
+            if (t <= rho) a += p; else b += p;
+          }
         }
       }
       tc_fence_before();
