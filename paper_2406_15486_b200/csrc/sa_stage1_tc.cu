@@ -187,11 +187,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         uint32_t r[32];
         tmem_ld32(taddr + ch * 32, r);
         tmem_ld_wait();
-        if (full) {  // same values and summation order as the masked loop, minus the mask
+        if (full) {  // same values (FFMA2 = two fused FMAs) and summation order as the masked loop
+          const uint64_t negm = f32x2(-m_new, -m_new), sl2x2 = f32x2(sl2, sl2);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float p = ex2(fmaf(__uint_as_float(r[i]), sl2, -m_new));
-            if (ch * 32 + i <= rho) a += p; else b += p;
+          for (int i = 0; i < 32; i += 2) {
+            float y0, y1;
+            unpack_f32x2(ffma2(f32x2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, negm), y0, y1);
+            const float p0 = ex2(y0), p1 = ex2(y1);
+            if (ch * 32 + i <= rho) a += p0; else b += p0;
+            if (ch * 32 + i + 1 <= rho) a += p1; else b += p1;
           }
         } else {
 #pragma unroll
