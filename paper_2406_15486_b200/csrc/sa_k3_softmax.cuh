@@ -25,7 +25,8 @@ struct K3Tile {
 
 struct K3TileBars {
   uint64_t* s_full;  // S(j) landed in TMEM           (tcgen05.commit)
-  uint64_t* p_part;  // P(j) keys 0..95 in TMEM        (128 arrivals; pair mode: 1 per CTA)
+  uint64_t* pv_half; // PV(j) over keys 0..63 done    (tcgen05.commit; split fast path only, may be null)
+  uint64_t* p_part;  // P(j) keys 0..63 (split fast path) / 0..95 in TMEM (128 arrivals; pair mode: 1 per CTA)
   uint64_t* p_full;  // P(j) complete                  (128 arrivals; pair mode: 1 per CTA)
   uint64_t* o_full;  // last PV done                   (tcgen05.commit)
 };
@@ -89,6 +90,11 @@ struct K3Prof {
 #ifndef SA_K3_EXPH
 #define SA_K3_EXPH 0
 #endif
+// Single-SM kernels: the fast path publishes P in two halves (keys 0..63, then
+// 64..127) so the PV MMA starts after half of the softmax (see k3_softmax_tile).
+#ifndef SA_K3_FASTSPLIT
+#define SA_K3_FASTSPLIT 1
+#endif
 // Single-read fast path for off-diagonal blocks (see k3_softmax_tile).
 #ifndef SA_K3_FAST
 #define SA_K3_FAST 1
@@ -139,6 +145,8 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
   };
   auto arrive_part = [&]() { arrive_on(b.p_part, pc.p_part_cl); };
   auto arrive_full = [&]() { arrive_on(b.p_full, pc.p_full_cl); };
+  // p_part covers keys 0..63 (chunks 0-1) with the split fast path, else keys 0..95
+  constexpr int kPartCh = (!kPair && SA_K3_FASTSPLIT) ? 1 : 2;
   int ia = 0, ib = 0;  // union walk (pair mode)
   int jj = 0;          // own blocks processed so far
   for (int j = 0;; ++j) {
@@ -184,7 +192,107 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
     // the check passes.  If any row's max exceeds m_ref + 8 (rare once the
     // heavy columns have been seen) S is still intact in TMEM and the block
     // falls through to the two-pass path below.
-    if (!first && !diag && SA_K3_EXP == 0) {
+    if (!kPair && SA_K3_FASTSPLIT && !first && !diag && SA_K3_EXP == 0) {
+      // Two halves of 64 keys: each is published (p_part, p_full) as soon as its
+      // exponentials pass the 2^8 check, so the first half of PV overlaps the
+      // softmax of the second.  A failure in the first half leaves S intact for
+      // the two-pass path; a failure in the second half (rare) waits until the
+      // first half's PV has landed in O, rescales O and the row sum to the new
+      // max and redoes keys 64..127 (their scores are still intact).
+      const int jb = jj - 1;  // own block index
+      bool done = false;
+      uint32_t pk[32];
+      uint64_t bacc0, bacc1;
+      auto half_exps = [&](int h, float m, float& ymax) {
+        const uint64_t negm = f32x2(-m, -m);
+        bacc0 = f32x2(0.f, 0.f);
+        bacc1 = f32x2(0.f, 0.f);
+        ymax = -INFINITY;
+        uint32_t buf[2][32];
+        tmem_ld32(tS + h * 64, buf[0]);
+        tmem_ld32(tS + h * 64 + 32, buf[1]);
+        tmem_ld_wait_regs(buf[0]);
+        tmem_ld_wait_regs(buf[1]);
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            float y0, y1;
+            unpack_f32x2(ffma2(f32x2(__uint_as_float(buf[ch][2 * t]), __uint_as_float(buf[ch][2 * t + 1])), sl2x2,
+                               negm),
+                         y0, y1);
+            ymax = fmax3(ymax, y0, y1);
+            const uint64_t pp = ((t & 3) >= 4 - SA_K3_POLY) ? ex2_poly2(y0, y1) : f32x2(ex2(y0), ex2(y1));
+            if (t & 1)
+              bacc1 = fadd2(bacc1, pp);
+            else
+              bacc0 = fadd2(bacc0, pp);
+            float p0, p1;
+            unpack_f32x2(pp, p0, p1);
+            pk[ch * 16 + t] = pack_bf16(p0, p1);
+          }
+        }
+      };
+      auto store_half = [&](int h) {  // bf16 P of keys 64h..64h+63 -> cols 32h..32h+31
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          uint32_t(&q)[16] = *reinterpret_cast<uint32_t(*)[16]>(&pk[ch * 16]);
+          tmem_st16(tS + h * 32 + ch * 16, q);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+      };
+      float ymax;
+      half_exps(0, m_ref, ymax);
+      if (!__any_sync(0xffffffffu, ymax > kK3RescaleThreshold)) {
+        store_half(0);
+        arrive_part();
+        lacc0 = fadd2(lacc0, bacc0);
+        lacc1 = fadd2(lacc1, bacc1);
+        half_exps(1, m_ref, ymax);
+        if (__any_sync(0xffffffffu, ymax > kK3RescaleThreshold)) {
+          k3_wait(b.pv_half, jb & 1);  // O now holds every PV up to this block's keys 0..63
+          tc_fence_after();
+          float mx = -INFINITY;
+#pragma unroll
+          for (int ch = 0; ch < 2; ++ch) {
+            uint32_t r[32];
+            tmem_ld32_sync(tS + 64 + ch * 32, r);
+#pragma unroll
+            for (int t = 0; t < 32; t += 2) mx = fmax3(mx, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
+          }
+          const float m_new = fmaxf(m_ref, mx * sl2);
+          const float f = ex2(m_ref - m_new);
+          const uint64_t f2 = f32x2(f, f);
+          lacc0 = fmul2(lacc0, f2);
+          lacc1 = fmul2(lacc1, f2);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t o[32];
+            tmem_ld32_sync(tO + ch * 32, o);
+#pragma unroll
+            for (int t = 0; t < 32; t += 2) {
+              float a, c;
+              unpack_f32x2(fmul2(f32x2(__uint_as_float(o[t]), __uint_as_float(o[t + 1])), f2), a, c);
+              o[t] = __float_as_uint(a);
+              o[t + 1] = __float_as_uint(c);
+            }
+            tmem_st32(tO + ch * 32, o);
+          }
+          m_ref = m_new;
+          half_exps(1, m_ref, ymax);  // with the row max of keys 64..127 every exponent is <= 0
+        }
+        store_half(1);
+        arrive_full();
+        lacc0 = fadd2(lacc0, bacc0);
+        lacc1 = fadd2(lacc1, bacc1);
+        done = true;
+      }
+      if (done) {
+        pf.stop(3);
+        continue;
+      }
+    } else if (!first && !diag && SA_K3_EXP == 0) {
       const uint64_t negm = f32x2(-m_ref, -m_ref);
       uint32_t pk[64];
       uint64_t bacc0 = f32x2(0.f, 0.f), bacc1 = f32x2(0.f, 0.f);
@@ -371,7 +479,7 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
           }
         }
         tmem_st16(tS + ch * 16, pk);
-        if (ch == 2) {  // keys 0..95 of P are in TMEM: let the PV MMA start
+        if (ch == kPartCh) {  // the first part of P is in TMEM: let the PV MMA start
           tmem_st_wait();
           tc_fence_before();
           arrive_part();

@@ -256,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 2)
       pf.flush(lane_id() == 0);
     }
   } else {
-    const K3TileBars bars{&sm->s_full, &sm->p_part, &sm->p_full, &sm->o_full};
+    const K3TileBars bars{&sm->s_full, nullptr, &sm->p_part, &sm->p_full, &sm->o_full};
     const K3PairCtx pc{To.list, To.n, mapa_shared(smem_u32(&sm->p_part), 0), mapa_shared(smem_u32(&sm->p_full), 0),
                        rank != 0};
     k3_softmax_tile<true>(Tm, bars, tS, tO, warp & 3, P.S, P.out, P.lse, P.touched, pc);

@@ -48,7 +48,8 @@ constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 128, true);
 
 struct __align__(8) ShareSmem {
   uint64_t q_full[2], k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full[2], p_part[2], p_full[2], o_full[2];  // split softmax: p_part/p_full = keys 0..63 / 64..127
+  uint64_t s_full[2], p_part[2], p_full[2], o_full[2];  // p_part/p_full = keys 0..63 / 64..127 (SA_K3_FASTSPLIT)
+  uint64_t pv_half[2];                                    // PV over keys 0..63 of the current block done
   uint32_t tmem_base;
 #if SA_K3_SPLIT
   float xchg[2][768];  // per tile: half-row maxima [parity][half][row] and the epilogue row sums
@@ -148,6 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm->p_part[x], 128);
       mbar_init(&sm->p_full[x], 128);
       mbar_init(&sm->o_full[x], 1);
+      mbar_init(&sm->pv_half[x], 1);
     }
     fence_mbar_init();
   }
@@ -226,11 +228,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       pf.stop(7);
       tc_fence_after();
       if (elect_one()) {
-        constexpr int kFirst = SA_K3_SPLIT ? 4 : 6;  // K-steps covered by the first P signal
+        constexpr int kFirst = (SA_K3_SPLIT || SA_K3_FASTSPLIT) ? 4 : 6;  // K-steps covered by the first P signal
 #pragma unroll
         for (int kk = 0; kk < kFirst; ++kk)
           umma_ts(tO[x], tS[x] + kk * 8, v_desc0 + ((s * kTileBytes + kk * 2048) >> 4), kIdescPV,
                   (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&sm->pv_half[x]);  // the softmax's rare second-half rescale waits for this
       }
       __syncwarp();
       pf.start();
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       pf.stop(6);
       tc_fence_after();
       if (elect_one()) {
-        constexpr int kFirst = SA_K3_SPLIT ? 4 : 6;
+        constexpr int kFirst = (SA_K3_SPLIT || SA_K3_FASTSPLIT) ? 4 : 6;
         constexpr uint32_t kSecondCol = SA_K3_SPLIT ? 32 : 0;  // split: P of keys 64..127 sits at cols 64..95
 #pragma unroll
         for (int kk = kFirst; kk < 8; ++kk)
@@ -309,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int x = warp < 8 ? 0 : 1;
     const K3Tile Tx = x ? T[1] : T[0];  // select, not a dynamically indexed (local-memory) array
     if (Tx.n > 0) {
-      const K3TileBars b{&sm->s_full[x], &sm->p_part[x], &sm->p_full[x], &sm->o_full[x]};
+      const K3TileBars b{&sm->s_full[x], &sm->pv_half[x], &sm->p_part[x], &sm->p_full[x], &sm->o_full[x]};
       k3_softmax_tile<false>(Tx, b, x ? tS[1] : tS[0], x ? tO[1] : tO[0], warp & 3, P.S, P.out, P.lse, P.touched);
     }
 #endif
