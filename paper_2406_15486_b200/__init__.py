@@ -15,7 +15,7 @@ from .config import ChunkPlan, SampledRange, SparseConfig, n_blocks, plan_chunks
 from .errors import GeneratorError, InfeasibleGridError, InputError, InternalInvariantError
 from .heads import AttentionHead, HeadBatch, HeadSet, check_finite
 from .masks import BlockMask, ChunkSelection, SelectedIndices
-from .pipeline import (ORACLE_CAP, HeadMetrics, MetricsReport, SampleAttentionResult, dense_attention,
+from .pipeline import (ORACLE_CAP, HeadMetrics, MetricsReport, SampleAttentionResult, cra_full, dense_attention,
                        run_pipeline, sample_attention)
 from . import tensor_io
 from .graph import SampleAttentionGraph
@@ -31,7 +31,7 @@ __all__ = [
     "GUARD_EPS", "GeneratorError", "HeadBatch", "HeadMetrics", "HeadSet", "InfeasibleGridError", "InputError",
     "InternalInvariantError", "MetricsReport", "SampleAttentionGraph", "ORACLE_CAP", "ReducedScores", "SampleAttentionResult",
     "SampledRange", "SampledScores", "SelectedIndices", "SparseConfig", "arg_topk", "block_reduce",
-    "check_finite", "dense_attention", "find_k", "flop_accounting", "merge_index", "n_blocks", "plan_chunks",
+    "check_finite", "cra_full", "dense_attention", "find_k", "flop_accounting", "merge_index", "n_blocks", "plan_chunks",
     "resolve_config", "run_pipeline", "sample_attention", "sample_attention_host", "sample_scores", "select", "select_and_merge",
     "sparse_attention",
 ]

@@ -24,7 +24,7 @@ from .masks import BlockMask
 from .stages import (FlopReport, block_reduce, flop_accounting, merge_index, sample_scores, select,
                      sparse_attention)
 
-__all__ = ["ORACLE_CAP", "HeadMetrics", "MetricsReport", "run_pipeline", "sample_attention",
+__all__ = ["ORACLE_CAP", "HeadMetrics", "MetricsReport", "cra_full", "run_pipeline", "sample_attention",
            "SampleAttentionResult", "dense_attention"]
 
 ORACLE_CAP = 8192
@@ -182,6 +182,27 @@ def _retained(p: torch.Tensor, rows: torch.Tensor, dense_mask: torch.Tensor, blk
     pad = nb * blk - S
     bs = torch.nn.functional.pad(p, (0, pad)).view(p.shape[0], nb, blk).sum(dim=2)
     return (bs * dense_mask[rows // blk]).sum(dim=1)
+
+
+def cra_full(batch: HeadBatch, mask: BlockMask, row_chunk: int = 1024) -> tuple:
+    """Entry-level CRA of every query row (ref oracle.py:86-99 / pipeline.py:37-58,
+    the reference's `cra_full`), on the GPU in fp64 and for any S -- the
+    reference caps it at ORACLE_CAP because it materialises S x S on the CPU;
+    here rows are processed `row_chunk` at a time.  Returns
+    per-head (min, mean) numpy arrays of the retained causal probability mass."""
+    S, blk = batch.S, mask.blk
+    dense = torch.from_numpy(mask.to_dense()).to(batch.q.device)
+    mins, means = [], []
+    for h in range(batch.Hq):
+        kh = batch.k[(batch.q_head0 + h) // batch.group - batch.q_head0 // batch.group]
+        kept = []
+        for r0 in range(0, S, row_chunk):
+            rows = torch.arange(r0, min(S, r0 + row_chunk), device=batch.q.device)
+            kept.append(_retained(_causal_probs(batch.q[h, rows], kh, rows), rows, dense[h], blk))
+        k_all = torch.cat(kept)
+        mins.append(float(k_all.min()))
+        means.append(float(k_all.mean()))
+    return np.array(mins), np.array(means)
 
 
 def run_pipeline(head_set, cfg: SparseConfig, want_oracle: bool = False, seed: int | None = None,

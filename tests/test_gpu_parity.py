@@ -363,3 +363,26 @@ def test_lse_matches_masked_logsumexp(sa, dtype):
         err = (res.lse[h].double() - ref).abs().max().item()
         assert err <= (2e-3 if dtype == "bf16" else 1e-5), (h, err)  # fp32 math: ~1e-7 relative on |lse| ~ 10
     assert nb == 8
+
+
+def test_cra_full_beyond_the_oracle_cap(sa):
+    """cra_full (entry-level retained mass of every row) on the GPU: equals
+    run_pipeline's oracle metric below ORACLE_CAP, runs beyond it, and is
+    exactly 1 for a full mask."""
+    from paper_2406_15486_b200 import synth
+
+    q, k, v, _ = synth.make_inputs(4096, 2, 1, 128, seed=2, device="cuda")
+    b = sa.HeadBatch.from_tensors(q, k, v)
+    cfg = sa.SparseConfig(0.9, 0.9, chunk_n=2)
+    rep = sa.run_pipeline(b, cfg, want_oracle=True)
+    _, res = sa.sample_attention(q, k, v, alpha=0.9, chunk_n=2)  # the same stages 1-2 as run_pipeline
+    mins, means = sa.cra_full(b, res.mask)
+    for h in range(2):
+        assert abs(mins[h] - rep.heads[h].cra_full_min) < 1e-12
+        assert abs(means[h] - rep.heads[h].cra_full_mean) < 1e-12
+    full_min, _ = sa.cra_full(b, sa.BlockMask.full(2, 4096, 128))
+    assert np.allclose(full_min, 1.0, atol=1e-12)
+    q2, k2, v2, _ = synth.make_inputs(16384, 1, 1, 128, seed=3, device="cuda")
+    _, res = sa.sample_attention(q2, k2, v2, alpha=0.95, chunk_n=1)
+    m16, a16 = sa.cra_full(sa.HeadBatch.from_tensors(q2, k2, v2), res.mask)
+    assert 0.0 < m16[0] <= a16[0] <= 1.0 + 1e-12
