@@ -233,10 +233,13 @@ def main():
     import paper_2406_15486_b200 as sa
     from paper_2406_15486_b200 import _lib, synth
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one process per GPU; more ranks than GPUs (a multi-rank smoke test on one GPU) wrap around
+    gpu = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("SA_DIST_BACKEND", "nccl")  # gloo: ranks sharing one GPU (tests only)
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     if Hq % world:
         raise SystemExit(f"{Hq} heads do not shard over {world} ranks")
     per = Hq // world
@@ -312,7 +315,7 @@ def main():
 
     # ---- timed region (device-resident inputs)
     step_ms, k3_ms, s1_ms, s2_ms = [], [], [], []
-    clk = ClockSampler(local_rank)
+    clk = ClockSampler(gpu)
     clk.start()
     launches0 = _lib.launch_count()
     barrier()
@@ -339,7 +342,11 @@ def main():
         gexec.check()
     t_step = sum(step_ms) / len(step_ms)
     t_local = torch.tensor([t_step], device=dev)
-    if world > 1:
+    per_rank_ms = [t_step]
+    if world > 1:  # per-rank step times (head-specific density makes ranks uneven), then the max
+        gathered = [torch.zeros_like(t_local) for _ in range(world)]
+        dist.all_gather(gathered, t_local)
+        per_rank_ms = [float(x.item()) for x in gathered]
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     t_max = float(t_local.item())
 
@@ -372,6 +379,8 @@ def main():
     extra = {"stage_ms": {"stage1": round(sum(s1_ms) / len(s1_ms), 3), "stage2": round(sum(s2_ms) / len(s2_ms), 3),
                           "stage3": round(t_k3, 3)},
              "filtering_overhead": round(1 - t_k3 / t_step, 4),
+             "per_rank_ms": [round(x, 3) for x in per_rank_ms],
+             "rank_imbalance": round(max(per_rank_ms) / (sum(per_rank_ms) / len(per_rank_ms)), 4),
              "block_density": round(flop.block_density, 4),
              "rescored_pairs": res.n_rescored(),
              "kept_tflop": round(kept / 1e12, 3), "dense_tflop": round(dense_job / world / 1e12, 3)}
