@@ -553,7 +553,8 @@ def run_reference(args, rank, S, Hq, Hkv, d, alpha, chunk_n, workload):
     ms = t_head * Hq * 1e3
     line = {"metric": "sparse prefill attention eff. TFLOP/s at 128K (ChatGLM3-6B shape, alpha=0.95)"
             if args.config == "c3" else f"sparse prefill attention eff. TFLOP/s ({args.config})",
-            "value": round(value, 5), "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "value": round(value, 5), "unit": "TFLOP/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+            "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 1), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (same seeded generator, head 0)", "config": workload,
             "impl": "reference",
