@@ -73,6 +73,9 @@ struct K3Prof {
 // Fraction of off-diagonal exponentials computed by the FMA-pipe polynomial:
 // SA_K3_POLY n -> n/4 (build-time knob; production 0: with P published in two
 // halves, all-MUFU exponentials measured ~4 % faster than a 1/4 polynomial share).
+#ifndef SA_K3_PREF  // fast path: issue the second half's TMEM loads before the first half's check/store
+#define SA_K3_PREF 0  // 1 measured 0.5 ms slower at C3
+#endif
 #ifndef SA_K3_POLY
 #define SA_K3_POLY 0
 #endif
@@ -203,14 +206,17 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
       bool done = false;
       uint32_t pk[32];
       uint64_t bacc0, bacc1;
-      auto half_exps = [&](int h, float m, float& ymax) {
+      uint32_t buf[2][32];
+      auto load_half = [&](int h) {
+        tmem_ld32(tS + h * 64, buf[0]);
+        tmem_ld32(tS + h * 64 + 32, buf[1]);
+      };
+      // exponentials of the half whose loads load_half() issued
+      auto half_exps = [&](float m, float& ymax) {
         const uint64_t negm = f32x2(-m, -m);
         bacc0 = f32x2(0.f, 0.f);
         bacc1 = f32x2(0.f, 0.f);
         ymax = -INFINITY;
-        uint32_t buf[2][32];
-        tmem_ld32(tS + h * 64, buf[0]);
-        tmem_ld32(tS + h * 64 + 32, buf[1]);
         tmem_ld_wait_regs(buf[0]);
         tmem_ld_wait_regs(buf[1]);
 #pragma unroll
@@ -243,13 +249,20 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
         tc_fence_before();
       };
       float ymax;
-      half_exps(0, m_ref, ymax);
+      load_half(0);
+      half_exps(m_ref, ymax);
+#if SA_K3_PREF
+      load_half(1);  // keys 64..127 stream in while half 0 is checked and stored
+#endif
       if (!__any_sync(0xffffffffu, ymax > kK3RescaleThreshold)) {
         store_half(0);
         arrive_part();
         lacc0 = fadd2(lacc0, bacc0);
         lacc1 = fadd2(lacc1, bacc1);
-        half_exps(1, m_ref, ymax);
+#if !SA_K3_PREF
+        load_half(1);
+#endif
+        half_exps(m_ref, ymax);
         if (__any_sync(0xffffffffu, ymax > kK3RescaleThreshold)) {
           k3_wait(b.pv_half, jb & 1);  // O now holds every PV up to this block's keys 0..63
           tc_fence_after();
@@ -280,7 +293,8 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
             tmem_st32(tO + ch * 32, o);
           }
           m_ref = m_new;
-          half_exps(1, m_ref, ymax);  // with the row max of keys 64..127 every exponent is <= 0
+          load_half(1);
+          half_exps(m_ref, ymax);  // with the row max of keys 64..127 every exponent is <= 0
         }
         store_half(1);
         arrive_full();
