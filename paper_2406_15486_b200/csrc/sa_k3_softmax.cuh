@@ -73,6 +73,9 @@ struct K3Prof {
 // Fraction of off-diagonal exponentials computed by the FMA-pipe polynomial:
 // SA_K3_POLY n -> n/4 (build-time knob; production 0: with P published in two
 // halves, all-MUFU exponentials measured ~4 % faster than a 1/4 polynomial share).
+#ifndef SA_K3_PVDRAIN  // wait on every pv_half phase (compute-sanitizer synccheck clean); 0: rare path only
+#define SA_K3_PVDRAIN 1
+#endif
 #ifndef SA_K3_PREF  // fast path: issue the second half's TMEM loads before the first half's check/store
 #define SA_K3_PREF 0  // 1 measured 0.5 ms slower at C3
 #endif
@@ -152,6 +155,7 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
   constexpr int kPartCh = (!kPair && SA_K3_FASTSPLIT) ? 1 : 2;
   int ia = 0, ib = 0;  // union walk (pair mode)
   int jj = 0;          // own blocks processed so far
+  int pv_seen = 0;     // pv_half phases consumed (split fast path)
   for (int j = 0;; ++j) {
     int kb;
     bool mine = true;
@@ -168,6 +172,14 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
       kb = __ldg(T.list + j);
     }
     const bool diag = kb == T.qb;  // warp-uniform
+#if SA_K3_PVDRAIN
+    if (!kPair && SA_K3_FASTSPLIT && pv_seen < jj) {
+      // consume the previous block's pv_half phase so that every phase has a waiter;
+      // it completes before this block's S (same tensor pipe), so the wait below hides it
+      k3_wait(b.pv_half, pv_seen & 1);
+      ++pv_seen;
+    }
+#endif
     pf.start();
     k3_wait(b.s_full, j & 1);
     pf.stop(0);
@@ -265,6 +277,7 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
         half_exps(m_ref, ymax);
         if (__any_sync(0xffffffffu, ymax > kK3RescaleThreshold)) {
           k3_wait(b.pv_half, jb & 1);  // O now holds every PV up to this block's keys 0..63
+          pv_seen = jb + 1;
           tc_fence_after();
           float mx = -INFINITY;
 #pragma unroll

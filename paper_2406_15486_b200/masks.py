@@ -125,8 +125,19 @@ class BlockMask:
 
     # ------------------------------------------------------------ host views
     def _host_csr(self):
+        """(kv_cnt, kv_idx) on the host.  Only the first kv_cnt entries of each
+        row segment are copied (a device gather); the capacity tail, which the
+        merge never writes, reads back as -1."""
         if self._host is None:
-            self._host = (self.kv_cnt.cpu().numpy(), self.kv_idx.cpu().numpy())
+            cnt = self.kv_cnt
+            nb, dev = self.n_qblocks, cnt.device
+            ar = torch.arange(nb, device=dev)
+            seg = torch.repeat_interleave(ar, ar + 1)                  # row of each slot
+            off = torch.arange(seg.numel(), device=dev) - seg * (seg + 1) // 2
+            valid = off[None, :] < cnt[:, seg]                          # [H, tri(nb)]
+            idx = np.full(tuple(self.kv_idx.shape), -1, dtype=np.int32)
+            idx[valid.cpu().numpy()] = self.kv_idx[valid].cpu().numpy()
+            self._host = (cnt.cpu().numpy(), idx)
         return self._host
 
     def _single(self):
@@ -175,7 +186,9 @@ class BlockMask:
         if self.k_sel is None:
             return None
         ks = self.k_sel.cpu().numpy()
-        ix = self.idx_sel.cpu().numpy()
+        valid = torch.arange(self.idx_sel.shape[-1], device=self.k_sel.device) < self.k_sel[..., None]
+        ix = np.full(tuple(self.idx_sel.shape), -1, dtype=np.int32)  # only the first k entries are written
+        ix[valid.cpu().numpy()] = self.idx_sel[valid].cpu().numpy()
         out = []
         for h in range(ks.shape[0]):
             chunks = []

@@ -22,4 +22,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
   timeout 300 python bench.py --steps 2 --warmup 3 --no-dense --no-cpu --no-e2e --no-graph > $OUT/ncu_launch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k3_share|k1_tc|k2_|xf_pass|s1_|k_check|k_flag" -s 0 -c 20 \
   -o $OUT/full timeout 600 python bench.py --steps 1 --warmup 3 --no-dense --no-cpu --no-e2e --no-graph > $OUT/ncu_full.log 2>&1
+mkdir -p $OUT/sanitizer
+for t in memcheck racecheck initcheck synccheck; do
+  timeout 400 compute-sanitizer --tool $t python -c "import __graft_entry__ as g; g.smoke()" > $OUT/sanitizer/$t.txt 2>&1
+done
 ls -la $OUT
