@@ -73,6 +73,9 @@ struct K3Prof {
 // Fraction of off-diagonal exponentials computed by the FMA-pipe polynomial:
 // SA_K3_POLY n -> n/4 (build-time knob; production 0: with P published in two
 // halves, all-MUFU exponentials measured ~4 % faster than a 1/4 polynomial share).
+#ifndef SA_K3_WARPARRIVE  // P-ready barriers: one arrive per softmax warp (count 4) instead of per thread (128)
+#define SA_K3_WARPARRIVE 1
+#endif
 #ifndef SA_K3_PVDRAIN  // wait on every pv_half phase (compute-sanitizer synccheck clean); 0: rare path only
 #define SA_K3_PVDRAIN 1
 #endif
@@ -146,7 +149,12 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
           mbar_arrive(local);
       }
     } else {
+#if SA_K3_WARPARRIVE
+      __syncwarp();  // every lane has waited for and fenced its TMEM stores
+      if (lane_id() == 0) mbar_arrive(local);
+#else
       mbar_arrive(local);
+#endif
     }
   };
   auto arrive_part = [&]() { arrive_on(b.p_part, pc.p_part_cl); };

@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm->v_full[x], 1);
       mbar_init(&sm->v_empty[x], 1);
       mbar_init(&sm->s_full[x], 1);
-      mbar_init(&sm->p_part[x], 128);
-      mbar_init(&sm->p_full[x], 128);
+      mbar_init(&sm->p_part[x], (SA_K3_WARPARRIVE && !SA_K3_SPLIT) ? 4 : 128);
+      mbar_init(&sm->p_full[x], (SA_K3_WARPARRIVE && !SA_K3_SPLIT) ? 4 : 128);
       mbar_init(&sm->o_full[x], 1);
       mbar_init(&sm->pv_half[x], 1);
     }
