@@ -35,6 +35,11 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+if "reference" in sys.argv and "--impl" in sys.argv:
+    # the CPU arm uses every host core for BLAS, also under torchrun (which sets OMP_NUM_THREADS=1);
+    # set before numpy loads OpenBLAS
+    _cores = str(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
+    os.environ["OPENBLAS_NUM_THREADS"] = os.environ["OMP_NUM_THREADS"] = _cores
 
 CONFIGS = {
     # name: (S, Hq, Hkv, alpha, chunk_n, description)
@@ -122,6 +127,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def k3_traffic(config, alpha, chunk_n, world, gather):
+    """DRAM bytes per K3 launch (dram__bytes_read.sum + dram__bytes_write.sum,
+    one ncu --set full capture) of THIS workload, from profiles/k3_traffic.json
+    (keyed by workload); None when that workload was not captured."""
+    try:
+        table = json.load(open(os.path.join(ROOT, "profiles", "k3_traffic.json")))
+    except (OSError, ValueError):
+        return None
+    key = f"{config}_a{alpha:.2f}_cn{chunk_n}_n{world}" + ("_gather" if gather else "")
+    entry = table.get("workloads", {}).get(key)
+    return entry.get("bytes_per_launch") if entry else None
+
+
 def dense_flops(S: int, d: int, blk: int = 128) -> int:
     """ref executor.py:65 for one head: 4*d*sum over causal block pairs of m*n."""
     nb = -(-S // blk)
@@ -131,8 +149,11 @@ def dense_flops(S: int, d: int, blk: int = 128) -> int:
 
 # ------------------------------------------------------------------ CPU side
 def cpu_sample(q, k, v, alpha, chunk_n, blk=128, n_qblocks=8, seed=0):
-    """Time the CPU oracle on one head: stage 1+2 in full, stage 3 on a seeded
-    sample of query blocks; returns per-head seconds (extrapolated) and detail."""
+    """Time the CPU oracle (the pinned numpy port of the reference path) on
+    one head: stage 1+2 in full, stage 3 (O.sparse_attention, the reference's
+    recurrence) on a seeded sample of query blocks.  Returns the measured
+    times, the extrapolation of stage 3 to the whole head, and the head's
+    selection / block grid (for the parity check against the GPU)."""
     import numpy as np
     from oracle import blocksift_port as O
 
@@ -147,40 +168,16 @@ def cpu_sample(q, k, v, alpha, chunk_n, blk=128, n_qblocks=8, seed=0):
     nb = grid.shape[0]
     rng = np.random.default_rng(seed)
     qbs = sorted(rng.choice(nb, size=min(n_qblocks, nb), replace=False).tolist())
-    blocks = 0
     t3 = time.perf_counter()
-    for qb in qbs:  # stage 3 restricted to the sampled query blocks (same recurrence)
-        _sparse_rows(O, q, k, v, grid, qb, blk)
-        blocks += int(grid[qb].sum())
+    _, blocks = O.sparse_attention(q, k, v, grid, blk, qblocks=qbs)
     t4 = time.perf_counter()
     total_blocks = int(grid.sum())
-    t_stage3 = (t4 - t3) * total_blocks / max(1, blocks)
-    return {"t_stage1": t1 - t0, "t_stage2": t2 - t1, "t_stage3_extrapolated": t_stage3,
-            "t_head": (t1 - t0) + (t2 - t1) + t_stage3, "sampled_qblocks": len(qbs),
-            "sampled_blocks": blocks, "head_blocks": total_blocks, "density": total_blocks / (nb * (nb + 1) / 2)}
-
-
-def _sparse_rows(O, q, k, v, grid, qb, blk):
-    import numpy as np
-
-    S, d = q.shape
-    a, b = qb * blk, min((qb + 1) * blk, S)
-    qs = q[a:b] * (1.0 / np.sqrt(d))
-    m = np.full(b - a, -np.inf)
-    l = np.zeros(b - a)
-    acc = np.zeros((b - a, d))
-    for kb in np.flatnonzero(grid[qb]):
-        c0, c1 = kb * blk, min((kb + 1) * blk, S)
-        z = qs @ k[c0:c1].T
-        if kb == qb:
-            z[np.arange(c0, c1)[None, :] > np.arange(a, b)[:, None]] = -np.inf
-        mn = np.maximum(m, z.max(axis=1))
-        corr = np.exp(m - mn)
-        pz = np.exp(z - mn[:, None])
-        l = corr * l + pz.sum(axis=1)
-        acc = acc * corr[:, None] + pz @ v[c0:c1]
-        m = mn
-    return acc / l[:, None]
+    factor = total_blocks / max(1, blocks)
+    t_stage3 = (t4 - t3) * factor
+    return {"t_stage1": t1 - t0, "t_stage2": t2 - t1, "t_stage3_sample": t4 - t3, "t_stage3_extrapolated": t_stage3,
+            "t_sample": t4 - t0, "t_head": (t1 - t0) + (t2 - t1) + t_stage3, "sampled_qblocks": len(qbs),
+            "sampled_blocks": blocks, "head_blocks": total_blocks, "stage3_extrapolation": round(factor, 2),
+            "density": total_blocks / (nb * (nb + 1) / 2), "selection": sel, "grid": grid}
 
 
 def cpu_threads() -> int:
@@ -207,8 +204,10 @@ def main():
     ap.add_argument("--chunk-n", type=int, default=None)
     ap.add_argument("--no-graph", action="store_true", help="launch the stages from Python instead of CUDA graphs")
     ap.add_argument("--gather", action="store_true", help="all-gather outputs over NCCL (default for c5)")
+    ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
-    args.warmup = max(3, args.warmup)
+    args.warmup = max(3, args.warmup) if not args.dry_run else args.warmup
+    maybe_spawn(args)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -224,6 +223,8 @@ def main():
                 "chunk_n": chunk_n, "blk": 128, "parallelism": f"heads/{world}" + ("+gather" if gather else ""),
                 "l2": "flushed between steps"}
 
+    if args.dry_run:
+        return dry_run(args, world, rank)
     if args.impl == "reference":
         return run_reference(args, rank, S, Hq, Hkv, d, alpha, chunk_n, workload)
 
@@ -294,7 +295,7 @@ def main():
             masks = []
 
             def fn(qq, kk, vv, **kw2):
-                o_, r_ = sa.sample_attention(qq, kk, vv, **kw2)
+                o_, r_ = sa.sample_attention(qq, kk, vv, check_inputs=False, **kw2)
                 masks.append(r_.mask)
                 return o_, r_
 
@@ -363,13 +364,7 @@ def main():
         t_k3 = t_step
     pk, pk_kind = peaks()
     achieved = kept / (t_k3 * 1e-3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "k3_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic = k3_traffic(args.config, alpha, chunk_n, world, gather)
     roof = {"bound": "tensor", "kernel": "k3_share (stage-3 sparse prefill, K/V-sharing units)", "achieved": round(achieved, 2),
             "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": round(achieved / pk["bf16_tflops"], 4),
             "frac_of_sustained": round(achieved / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]), 4),
@@ -413,7 +408,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(q, k, v, kv_heads, group, alpha, chunk_n, S, d)
+        cpu = cpu_baseline(q, k, v, kv_heads, group, alpha, chunk_n, S, d, mask=res.mask)
 
     if rank == 0:
         line = {"metric": "sparse prefill attention eff. TFLOP/s at 128K (ChatGLM3-6B shape, alpha=0.95)"
@@ -516,25 +511,42 @@ def e2e_run(sa, q, k, v, alpha, chunk_n, group, q_head0, args, dev, world, dense
             "path": "sample_attention_host (pinned host q/k/v -> pinned host out, copies overlapped)"}
 
 
-def cpu_baseline(q, k, v, kv_heads, group, alpha, chunk_n, S, d):
-    """CPU oracle on head 0 (stage 1+2 full, stage 3 sampled), extrapolated."""
+def cpu_baseline(q, k, v, kv_heads, group, alpha, chunk_n, S, d, mask=None):
+    """CPU oracle on head 0 (stage 1+2 full, stage 3 sampled), extrapolated;
+    with `mask` (the GPU's BlockMask of the timed step) the oracle's head-0
+    selection and block grid are compared with the GPU's: parity_head0."""
+    import numpy as np
+
     qh = q[0].double().cpu().numpy()
     kh = k[kv_heads.index(0 // group)].double().cpu().numpy()
     vh = v[kv_heads.index(0 // group)].double().cpu().numpy()
     r = cpu_sample(qh, kh, vh, alpha, chunk_n)
     val = dense_flops(S, d) / r["t_head"] / 1e12
-    return {"value": round(val, 5), "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
-            "sample": (f"head 0 of the same workload: stage 1+2 in full ({r['t_stage1'] + r['t_stage2']:.2f} s), "
-                       f"stage 3 on {r['sampled_qblocks']} seeded query blocks ({r['sampled_blocks']} of "
-                       f"{r['head_blocks']} kept blocks) extrapolated to the head ({r['t_stage3_extrapolated']:.1f} s); "
-                       f"per-head time {r['t_head']:.1f} s, every head costs the same"),
-            "density_head0": round(r["density"], 4)}
+    out = {"value": round(val, 5), "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
+           "sample": _sample_text(r), "density_head0": round(r["density"], 4)}
+    if mask is not None:
+        got = [(c.i_c, c.i_s) for c in mask.selections()[0].chunks]
+        want = [(tuple(a), tuple(b)) for a, b in r["selection"]]
+        out["parity_head0"] = bool(got == want and np.array_equal(mask.head(0).to_dense()[0], r["grid"]))
+    return out
+
+
+def _sample_text(r):
+    return (f"head 0 of the same workload: stage 1+2 in full ({r['t_stage1'] + r['t_stage2']:.2f} s), "
+            f"stage 3 (oracle sparse_attention) on {r['sampled_qblocks']} seeded query blocks "
+            f"({r['sampled_blocks']} of {r['head_blocks']} kept blocks, {r['t_stage3_sample']:.2f} s) extrapolated "
+            f"x{r['stage3_extrapolation']} to the head ({r['t_stage3_extrapolated']:.1f} s); "
+            f"per-head time {r['t_head']:.1f} s, every head costs the same")
 
 
 def run_reference(args, rank, S, Hq, Hkv, d, alpha, chunk_n, workload):
-    """--impl reference: the reference's CPU algorithm (the pinned numpy port)
-    timed on this host, rank 0 only; every step is a bounded sample of the
-    workload (one head, stage 3 sampled) extrapolated per head."""
+    """--impl reference: the reference's CPU algorithm (the oracle, a numpy
+    port pinned to the reference's own outputs) timed on this host, rank 0
+    only.  Every step is the SAME bounded sample the cpu_baseline leg of our
+    arm times (head 0: stage 1+2 in full, stage 3 on 8 seeded query blocks),
+    so the two CPU numbers describe one measurement.  ms_per_step is what
+    actually ran; value extrapolates stage 3 to the head (factor in the line)
+    and is per head, which is the job's rate too: every head costs the same."""
     if rank != 0:
         return
     import torch
@@ -543,26 +555,74 @@ def run_reference(args, rank, S, Hq, Hkv, d, alpha, chunk_n, workload):
 
     q, k, v, kv = synth.make_inputs(S, Hq, Hkv, d, seed=args.seed, heads=[0], device="cpu")
     qh, kh, vh = (t[0].double().numpy() for t in (q, k, v))
-    ts = []
+    runs = []
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(qh, kh, vh, alpha, chunk_n, n_qblocks=4, seed=i)
+        r = cpu_sample(qh, kh, vh, alpha, chunk_n)
         if i >= args.warmup:
-            ts.append(r["t_head"])
-    t_head = sum(ts) / len(ts)
+            runs.append(r)
+    t_sample = sum(r["t_sample"] for r in runs) / len(runs)
+    t_head = sum(r["t_head"] for r in runs) / len(runs)
     value = dense_flops(S, d) / t_head / 1e12
-    ms = t_head * Hq * 1e3
+    r = runs[-1]
     line = {"metric": "sparse prefill attention eff. TFLOP/s at 128K (ChatGLM3-6B shape, alpha=0.95)"
             if args.config == "c3" else f"sparse prefill attention eff. TFLOP/s ({args.config})",
             "value": round(value, 5), "unit": "TFLOP/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms, 1), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (same seeded generator, head 0)", "config": workload,
-            "impl": "reference",
+            "ms_per_step": round(t_sample * 1e3, 1), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (same seeded generator, head 0)",
+            "config": workload, "impl": "reference",
+            "step": "one bounded sample per step (what ms_per_step times): " + _sample_text(r),
+            "extrapolation": {"stage3_factor": r["stage3_extrapolation"], "ms_per_head": round(t_head * 1e3, 1),
+                              "ms_per_job_extrapolated": round(t_head * Hq * 1e3, 1), "heads": Hq},
             "cpu_baseline": {"value": round(value, 5), "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
-                             "sample": "per step: head 0, stage 1+2 full, stage 3 on 4 seeded query blocks, "
-                                       "extrapolated to 32 heads"},
+                             "sample": _sample_text(r)},
             "e2e": {"value": round(value, 5), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def maybe_spawn(args) -> None:
+    """`--gpus N` without a torchrun environment: re-launch this command as N
+    ranks (one process per GPU) through torch.distributed.run on 127.0.0.1;
+    the exit code is torchrun's."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def dry_run(args, world, rank):
+    """--dry-run: the multi-rank launch, barrier, per-rank timing gather and
+    max-over-ranks reduction of the real run, on CPU over gloo, with a no-op
+    step (a fixed sleep) in place of the kernels.  Test-only plumbing check."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        time.sleep(0.01 * (1 + rank))
+        ts.append((time.perf_counter() - t0) * 1e3)
+    t_step = sum(ts) / len(ts)
+    per_rank = [t_step]
+    if world > 1:
+        g = [torch.zeros(1) for _ in range(world)]
+        dist.all_gather(g, torch.tensor([t_step]))
+        per_rank = [float(x.item()) for x in g]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "steps": args.steps, "ms_per_step": round(max(per_rank), 3),
+                          "per_rank_ms": [round(x, 3) for x in per_rank]}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -65,6 +65,18 @@ const char* sa_last_error(void);
  * (monotonic; the bench reports deltas as gpu_launches). */
 long long sa_launch_count(void);
 
+/* Device-side invariant status of the calling thread's current device,
+ * accumulated by sa_sparse_forward since the last reset (synchronises the
+ * device).  status4[0] is the OR of SA_STATUS_* bits, status4[1] / [2] the
+ * head and query block of the first report, status4[3] the report count.
+ * Replaces the executor's raises (executor.py:131-132 InputError for a query
+ * block without active key blocks, :150-153 InternalInvariantError for an
+ * empty normaliser) and the BlockMask invariants (filtering.py:97-106). */
+#define SA_STATUS_EMPTY_BLOCK 1u  /* InputError */
+#define SA_STATUS_MASK 2u         /* kb > qb, unsorted list or no diagonal: InternalInvariantError */
+#define SA_STATUS_NORMALISER 4u   /* l <= 0 or not finite: InternalInvariantError */
+int sa_status(unsigned* status4, int reset);
+
 /* Bytes of scratch the stage-1/2/3 calls need for this geometry. */
 size_t sa_workspace_bytes(int S, int Hq, int Hkv, int d, int blk, int chunk_n, int dtype);
 

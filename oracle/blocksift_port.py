@@ -44,6 +44,7 @@ __all__ = [
     "serialize_mask",
     "sampled_cra",
     "run_head",
+    "block_scores",
 ]
 
 
@@ -208,11 +209,14 @@ def select_and_merge(cols, slashes, plan: Plan, alpha_c: float, alpha_s: float):
     return sel, merge_index(sel, plan)
 
 
-def sparse_attention(q, k, v, grid: np.ndarray, blk: int):
+def sparse_attention(q, k, v, grid: np.ndarray, blk: int, qblocks=None):
     """Block-sparse causal attention with the online softmax recurrence;
     ref executor.py:104-158.  Per query block, active key blocks ascend;
     entry-level causality only inside the diagonal block; the logits are
     (q * (1/sqrt(d))) @ k^T as in ref executor.py:124,133,139.
+    qblocks: optional subset of query blocks to compute (the recurrence is
+    per query block, so a subset is exactly those rows of the full result;
+    other rows are NaN) -- for bounded CPU samples at full scale.
     Returns (out[S, d] fp64, touched_blocks)."""
     q = np.asarray(q, np.float64)
     k = np.asarray(k, np.float64)
@@ -220,9 +224,9 @@ def sparse_attention(q, k, v, grid: np.ndarray, blk: int):
     S, d = q.shape
     nb = n_blocks(S, blk)
     scale = 1.0 / np.sqrt(d)
-    out = np.empty((S, d))
+    out = np.full((S, d), np.nan) if qblocks is not None else np.empty((S, d))
     touched = 0
-    for qb in range(nb):
+    for qb in (range(nb) if qblocks is None else sorted(qblocks)):
         a, b = qb * blk, min((qb + 1) * blk, S)
         qs = q[a:b] * scale
         m = np.full(b - a, -np.inf)
@@ -308,3 +312,30 @@ def run_head(q, k, v, alpha_c: float, alpha_s: float, chunk_n: int, blk: int = 1
         res["out"] = out
         res["touched"] = touched
     return res
+
+
+def block_scores(q, k, plan: Plan, blk: int, workers: int | None = None):
+    """sampled_probs + block_reduce window by window, windows in parallel
+    threads (numpy releases the GIL), each window's probability rows freed
+    once reduced: the same arithmetic as the two functions above (same
+    per-window code, so the same fp64 results), with memory bounded by
+    `workers` windows instead of all of them (ref sampler.py:135-191 keeps
+    every [rows x S] window alive; at 96K and 77 windows that is 7.7 GB).
+    Returns (cols, slashes, totals) like block_reduce."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    S = q.shape[0]
+    q = np.asarray(q, np.float64)
+    k = np.asarray(k, np.float64)
+
+    def one(w):
+        a, b, _, _ = w
+        rows = np.arange(a, b)
+        cols, slashes, totals = block_reduce([(rows, _causal_softmax(_scores(q[a:b], k), rows))], S, blk)
+        return cols[0], slashes[0], totals[0]
+
+    n = workers or min(16, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else 4)
+    with ThreadPoolExecutor(max_workers=max(1, n)) as ex:
+        res = list(ex.map(one, plan.windows))
+    return [r[0] for r in res], [r[1] for r in res], [r[2] for r in res]

@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("SA_LIB_PATH") or os.path.join(os.path.dirname(os.path
 
 SA_OK, SA_ERR_INVALID, SA_ERR_UNSUPPORTED, SA_ERR_INTERNAL, SA_ERR_CUDA = 0, -1, -2, -3, -4
 SA_BF16, SA_FP32 = 0, 1
+SA_STATUS_EMPTY_BLOCK, SA_STATUS_MASK, SA_STATUS_NORMALISER = 1, 2, 4
 SA_STAGE1_TENSOR, SA_STAGE1_EXACT = 0, 1
 
 _P = ctypes.c_void_p
@@ -30,6 +31,7 @@ SIGNATURES = {
     "sa_version": (_I, []),
     "sa_last_error": (ctypes.c_char_p, []),
     "sa_launch_count": (_L, []),
+    "sa_status": (_I, [ctypes.POINTER(ctypes.c_uint), _I]),
     "sa_workspace_bytes": (_Z, [_I, _I, _I, _I, _I, _I, _I]),
     "sa_check_finite": (_I, [_P, _I, ctypes.c_int64, _P, _P]),
     "sa_stage1": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _Z, _P]),

@@ -27,10 +27,7 @@ SOURCES = [
     "sa_stage1_exact.cu",
     "sa_stage1_tc.cu",
     "sa_stage2.cu",
-    "sa_sparse_tc.cu",
     "sa_sparse_share.cu",
-    "sa_sparse_pair.cu",
-    "sa_sparse_half.cu",
     "sa_sparse_simt.cu",
 ]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

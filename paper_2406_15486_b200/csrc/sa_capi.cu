@@ -12,6 +12,8 @@
 #include <cstdlib>
 #include <atomic>
 #include <mutex>
+#include <set>
+#include <tuple>
 #include <string>
 
 #include "sa_internal.h"
@@ -60,6 +62,33 @@ int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
   return SA_OK;
+}
+
+__device__ unsigned g_status[4];
+
+unsigned* status_ptr() {
+  static std::mutex mu;
+  static unsigned* ptr[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ptr[dev & 63]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_status) != cudaSuccess) return nullptr;
+    ptr[dev & 63] = static_cast<unsigned*>(p);
+  }
+  return ptr[dev & 63];
+}
+
+void set_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(fn, dev, bytes);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(key)) return;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess) done.insert(key);
 }
 
 bool make_tmap_bf16_hsd(CUtensorMap* map, const void* base, int H, int S, int d, int box_rows) {
@@ -129,6 +158,18 @@ int sa_version(void) { return 100; }
 const char* sa_last_error(void) { return g_err.c_str(); }
 
 long long sa_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int sa_status(unsigned* status4, int reset) {
+  if (!status4) return fail(SA_ERR_INVALID, "sa_status: null pointer");
+  if (cudaMemcpyFromSymbol(status4, g_status, 4 * sizeof(unsigned)) != cudaSuccess)
+    return fail(SA_ERR_CUDA, "sa_status: cannot read the device status word");
+  if (reset) {
+    const unsigned z[4] = {0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(g_status, z, sizeof(z)) != cudaSuccess)
+      return fail(SA_ERR_CUDA, "sa_status: cannot reset the device status word");
+  }
+  return SA_OK;
+}
 
 size_t sa_workspace_bytes(int S, int Hq, int Hkv, int d, int blk, int chunk_n, int dtype) {
   if (S < 1 || Hq < 1 || blk < 1 || chunk_n < 1) return 0;
@@ -215,20 +256,6 @@ int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, in
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int n_order = order ? 2 * n_units(Hq, ceil_div(S, blk), group, q_head0) : 0;
   if (dtype == SA_BF16) {
-    static const int impl = [] {
-      const char* e = getenv("SA_K3_IMPL");
-      if (e && e[0] == 's') return 1;  // "single": one item per CTA, two CTAs per SM (no K/V sharing)
-      if (e && e[0] == 'p') return 2;  // "pair": units over SM pairs (cta_group::2)
-      if (e && e[0] == 'h') return 3;  // "half": units with half-block S buffers
-      return 0;                        // "share": units in one CTA
-    }();
-    if (impl == 3)
-      return launch_sparse_half(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse, touched, st);
-    if (impl == 2)
-      return launch_sparse_pair(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse, touched, st);
-    if (impl == 1)
-      return launch_sparse_tc(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, n_order, out, lse,
-                              touched, st);
     return launch_sparse_share(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse, touched,
                                st);
   }

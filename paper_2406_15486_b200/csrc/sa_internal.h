@@ -15,6 +15,22 @@ namespace sa {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int check_launch(const char* what);
+// Opt `fn` into `bytes` of dynamic shared memory on the CURRENT device.  The
+// attribute is per device, so the opt-in is cached per (kernel, device, size).
+void set_smem_attr(const void* fn, int bytes);
+
+// Device status word behind sa_status(): [0] OR of the SA_STATUS_* bits,
+// [1] head and [2] query block of the first report, [3] number of reports
+// (bits SA_STATUS_EMPTY_BLOCK / _MASK / _NORMALISER, include/sampleattn.h).
+unsigned* status_ptr();  // this device's status word
+__device__ __forceinline__ void report_status(unsigned* st, unsigned bits, int h, int qb) {
+  if (!st) return;
+  atomicOr(st, bits);
+  if (atomicAdd(st + 3, 1u) == 0) {
+    st[1] = (unsigned)h;
+    st[2] = (unsigned)qb;
+  }
+}
 
 constexpr int kBlk = 128;       // tensor-core tile (query rows == key rows == blk)
 constexpr int kHeadDim = 128;   // tensor-core head dimension
@@ -59,10 +75,6 @@ int launch_flag_compact(const int* only, int n, int* list, cudaStream_t st);
 // grid rows used for flagged-pair loops (enough to fill the GPU, bounded by the pair count)
 inline int flagged_grid_rows(int n_pairs) { return n_pairs < 32 ? n_pairs : 32; }
 
-int launch_sparse_tc(const void* q, const void* k, const void* v, int S, int Hq, int Hkv,
-                     int group, int q_head0, const int* kv_cnt, const int* kv_idx,
-                     const int* order, int n_order, void* out, float* lse, long long* touched,
-                     cudaStream_t st);
 int launch_sparse_simt(const float* q, const float* k, const float* v, int S, int Hq, int Hkv,
                        int d, int blk, int group, int q_head0, const int* kv_cnt,
                        const int* kv_idx, const int* order, int n_order, float* out, float* lse,
@@ -115,12 +127,6 @@ __host__ __device__ inline int n_units(int Hq, int nb, int group, int q_head0) {
   return total;
 }
 
-int launch_sparse_pair(const void* q, const void* k, const void* v, int S, int Hq, int Hkv, int group,
-                       int q_head0, const int* kv_cnt, const int* kv_idx, const int* units, void* out,
-                       float* lse, long long* touched, cudaStream_t st);
-int launch_sparse_half(const void* q, const void* k, const void* v, int S, int Hq, int Hkv, int group,
-                       int q_head0, const int* kv_cnt, const int* kv_idx, const int* units, void* out,
-                       float* lse, long long* touched, cudaStream_t st);
 int launch_sparse_share(const void* q, const void* k, const void* v, int S, int Hq, int Hkv, int group,
                         int q_head0, const int* kv_cnt, const int* kv_idx, const int* units, void* out,
                         float* lse, long long* touched, cudaStream_t st);

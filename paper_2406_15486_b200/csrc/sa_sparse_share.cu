@@ -33,13 +33,8 @@ namespace sa {
 namespace {
 
 // warp 0 TMA, warp 1 MMA, warps 2-3 idle (so each softmax warpgroup starts at
-// TMEM lane quadrant 0), then the softmax warps: 4-7 for A and 8-11 for B, or
-// with SA_K3_SPLIT two warps per lane quadrant: 4-11 for A, 12-19 for B
-// (k3_softmax_split; more than 16 warps caps ptxas at 96 registers).
-#ifndef SA_K3_SPLIT
-#define SA_K3_SPLIT 0
-#endif
-constexpr int kWarps = SA_K3_SPLIT ? 20 : 12;
+// TMEM lane quadrant 0), then the softmax warps: 4-7 for A and 8-11 for B.
+constexpr int kWarps = 12;
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kTileBytes = 128 * 128 * 2;
 constexpr uint32_t kBoxBytes = kTileBytes / 2;
@@ -48,13 +43,9 @@ constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 128, true);
 
 struct __align__(8) ShareSmem {
   uint64_t q_full[2], k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full[2], p_part[2], p_full[2], o_full[2];  // p_part/p_full = keys 0..63 / 64..127 (SA_K3_FASTSPLIT)
+  uint64_t s_full[2], p_part[2], p_full[2], o_full[2];  // p_part/p_full = P of keys 0..63 / all keys
   uint64_t pv_half[2];                                    // PV over keys 0..63 of the current block done
   uint32_t tmem_base;
-#if SA_K3_SPLIT
-  float xchg[2][768];  // per tile: half-row maxima [parity][half][row] and the epilogue row sums
-  int flags[2][16];    // per tile: max-growth votes [parity][half][quad]
-#endif
 };
 
 struct ShareParams {
@@ -65,6 +56,7 @@ struct ShareParams {
   __nv_bfloat16* out;
   float* lse;
   long long* touched;
+  unsigned* status;
 };
 
 __device__ __forceinline__ K3Tile tile_of_item(const ShareParams& P, int item) {
@@ -146,8 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm->v_full[x], 1);
       mbar_init(&sm->v_empty[x], 1);
       mbar_init(&sm->s_full[x], 1);
-      mbar_init(&sm->p_part[x], (SA_K3_WARPARRIVE && !SA_K3_SPLIT) ? 4 : 128);
-      mbar_init(&sm->p_full[x], (SA_K3_WARPARRIVE && !SA_K3_SPLIT) ? 4 : 128);
+      mbar_init(&sm->p_part[x], 4);  // one arrive per softmax warp
+      mbar_init(&sm->p_full[x], 4);
       mbar_init(&sm->o_full[x], 1);
       mbar_init(&sm->pv_half[x], 1);
     }
@@ -216,19 +208,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     int kb;
     bool in[2];
     int t = 0;
-    // O_X += P_X V(step): keys 0..95 once that part of P is in TMEM, 96..127 after
+    // O_X += P_X V(step): keys 0..63 once that half of P is in TMEM, 64..127 after
     auto issue_pv = [&](int x, int step) {
       const int j = n_pv[x];
       const int s = step & 1;
       pf.start();
-      k3_wait(&sm->p_part[x], j & 1);  // (split softmax: keys 0..63)
+      k3_wait(&sm->p_part[x], j & 1);
       pf.stop(5);
       pf.start();
       k3_wait(&sm->v_full[s], (step >> 1) & 1);
       pf.stop(7);
       tc_fence_after();
       if (elect_one()) {
-        constexpr int kFirst = (SA_K3_SPLIT || SA_K3_FASTSPLIT) ? 4 : 6;  // K-steps covered by the first P signal
+        constexpr int kFirst = 4;  // K-steps (16 keys each) covered by p_part
 #pragma unroll
         for (int kk = 0; kk < kFirst; ++kk)
           umma_ts(tO[x], tS[x] + kk * 8, v_desc0 + ((s * kTileBytes + kk * 2048) >> 4), kIdescPV,
@@ -241,11 +233,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       pf.stop(6);
       tc_fence_after();
       if (elect_one()) {
-        constexpr int kFirst = (SA_K3_SPLIT || SA_K3_FASTSPLIT) ? 4 : 6;
-        constexpr uint32_t kSecondCol = SA_K3_SPLIT ? 32 : 0;  // split: P of keys 64..127 sits at cols 64..95
+        constexpr int kFirst = 4;
 #pragma unroll
         for (int kk = kFirst; kk < 8; ++kk)
-          umma_ts(tO[x], tS[x] + kSecondCol + kk * 8,
+          umma_ts(tO[x], tS[x] + kk * 8,
                   v_desc0 + ((s * kTileBytes + kk * 2048) >> 4), kIdescPV, 1u);
         if (j == T[x].n - 1) umma_commit(&sm->o_full[x]);
       }
@@ -298,24 +289,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     pf.flush(lane_id() == 0);
   } else if (warp >= 4) {
-#if SA_K3_SPLIT
-    const int x = warp < 12 ? 0 : 1;
-    const int half = (warp >> 2) & 1;  // warps 4-7 / 12-15: keys 0..63; 8-11 / 16-19: keys 64..127
-    const int quad = warp & 3;
-    const K3Tile Tx = x ? T[1] : T[0];
-    if (Tx.n > 0) {
-      const K3SplitBars b{&sm->s_full[x], &sm->p_part[x], &sm->p_full[x], &sm->o_full[x]};
-      k3_softmax_split(Tx, b, x ? tS[1] : tS[0], x ? tO[1] : tO[0], quad, half, sm->xchg[x], sm->flags[x],
-                       1 + x * 4 + quad, P.S, P.out, P.lse, P.touched);
-    }
-#else
     const int x = warp < 8 ? 0 : 1;
     const K3Tile Tx = x ? T[1] : T[0];  // select, not a dynamically indexed (local-memory) array
     if (Tx.n > 0) {
       const K3TileBars b{&sm->s_full[x], &sm->pv_half[x], &sm->p_part[x], &sm->p_full[x], &sm->o_full[x]};
-      k3_softmax_tile<false>(Tx, b, x ? tS[1] : tS[0], x ? tO[1] : tO[0], warp & 3, P.S, P.out, P.lse, P.touched);
+      k3_softmax_tile(Tx, b, x ? tS[1] : tS[0], x ? tO[1] : tO[0], warp & 3, P.S, P.out, P.lse, P.touched, P.status);
+    } else if ((x ? ib : ia) >= 0 && warp == 4 + 4 * x && lane_id() == 0) {
+      report_status(P.status, SA_STATUS_EMPTY_BLOCK, Tx.h, Tx.qb);  // ref executor.py:131-132
     }
-#endif
   }
   tc_fence_before();
   __syncthreads();
@@ -346,12 +327,9 @@ int launch_sparse_share(const void* q, const void* k, const void* v, int S, int 
   P.out = static_cast<__nv_bfloat16*>(out);
   P.lse = lse;
   P.touched = touched;
+  P.status = status_ptr();
   const size_t smem = 6 * (size_t)kTileBytes + sizeof(ShareSmem) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k3_share, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  set_smem_attr(reinterpret_cast<const void*>(&k3_share), (int)smem);
   if (touched) cudaMemsetAsync(touched, 0, sizeof(long long) * Hq, st);
   const int nu = n_units(Hq, P.nb, group, q_head0);
   k3_share<<<nu, kThreads, smem, st>>>(tq, tk, tv, P);

@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(128)
     k3_simt(const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
             int S, int d, int blk, int nb, int group, int q_head0, const int* __restrict__ kv_cnt,
             const int* __restrict__ kv_idx, const int* __restrict__ order, float* __restrict__ out,
-            float* __restrict__ lse, long long* __restrict__ touched) {
+            float* __restrict__ lse, long long* __restrict__ touched, unsigned* status) {
   extern __shared__ float sm_f[];
   float (*ks)[DP + 1] = reinterpret_cast<float (*)[DP + 1]>(sm_f);
   float (*vs)[DP + 1] = reinterpret_cast<float (*)[DP + 1]>(sm_f + kChunk * (DP + 1));
@@ -45,8 +45,11 @@ __global__ void __launch_bounds__(128)
   float m = -INFINITY, l = 0.f;
   const float* kh = k + (size_t)kvh * S * d;
   const float* vh = v + (size_t)kvh * S * d;
+  if (n == 0 && threadIdx.x == 0) report_status(status, SA_STATUS_EMPTY_BLOCK, h, qb);  // executor.py:131-132
+  bool bad_list = n > 0 && list[n - 1] != qb;  // BlockMask invariants, filtering.py:97-106
   for (int j = 0; j < n; ++j) {
     const int kb = list[j];
+    bad_list |= kb > qb || (j > 0 && kb <= list[j - 1]);
     const int k0 = kb * blk, k1 = min(k0 + blk, S);
     for (int c0 = k0; c0 < k1; c0 += kChunk) {
       const int cn = min(kChunk, k1 - c0);
@@ -86,6 +89,8 @@ __global__ void __launch_bounds__(128)
       m = m_new;
     }
   }
+  if (threadIdx.x == 0 && bad_list) report_status(status, SA_STATUS_MASK, h, qb);
+  if (valid && n > 0 && !(l > 0.f && l < INFINITY)) report_status(status, SA_STATUS_NORMALISER, h, qb);
   if (valid) {
     const float inv = 1.f / l;
     for (int c = 0; c < d; ++c) out[((size_t)h * S + row) * d + c] = acc[c] * inv;
@@ -110,7 +115,7 @@ int launch_sparse_simt(const float* q, const float* k, const float* v, int S, in
   cudaFuncSetAttribute(k3_simt<DPV>, cudaFuncAttributeMaxDynamicSharedMemorySize,               \
                        (int)((2 * kChunk + threads) * (DPV + 1) * sizeof(float)));               \
   k3_simt<DPV><<<grid, threads, (2 * kChunk + threads) * (DPV + 1) * sizeof(float), st>>>(q, k, v, S, d, blk, nb, group, q_head0, kv_cnt, kv_idx, \
-                                         order, out, lse, touched); \
+                                         order, out, lse, touched, status_ptr()); \
   } while (0)
   if (d <= 8)
     SA_SIMT_CASE(8);

@@ -460,11 +460,7 @@ template <typename T>
 int run_exact(const Stage1Geom& g, const T* q, const T* k, const int* only, char* ws, const Workspace& L,
               double* col, double* slash, cudaStream_t st) {
   const size_t smem = (size_t)(kRows + kKeys) * (SA_XF_DMMA ? kPitchD : kDChunk + 1) * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(xf_pass<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
-  }
+  set_smem_attr(reinterpret_cast<const void*>(&xf_pass<T>), (int)smem);
   const size_t plane = (size_t)g.Hq * g.cn * g.blk * g.nb;
   double* pa = reinterpret_cast<double*>(ws + L.x_part);
   double* pb = pa + plane;

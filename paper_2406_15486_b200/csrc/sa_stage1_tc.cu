@@ -244,11 +244,7 @@ int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const in
   P.kb_per_cta = kpc;
   const int nsplit = ceil_div(g.nb, kpc);
   const size_t smem = kTileBytes * (1 + kStages) + sizeof(K1Smem) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  set_smem_attr(reinterpret_cast<const void*>(&k1_tc), (int)smem);
   k1_tc<<<dim3(nsplit, g.Hq * g.cn), kThreads, smem, st>>>(tq, tk, P);
   if (int e = check_launch("stage1 tcgen05")) return e;
   return launch_fold<float, true>(g, only, P.pa, P.pb, P.pm, ws, L, col, slash, st);

@@ -22,7 +22,7 @@ import torch
 from . import _lib
 from .config import plan_chunks, resolve_config
 from .errors import InputError
-from .heads import HeadBatch, check_finite_async
+from .heads import HeadBatch, check_finite_async, raise_on_flags
 from .stages import block_reduce, merge_index, private_workspace, sample_scores, select, sparse_attention
 
 __all__ = ["SampleAttentionGraph"]
@@ -99,9 +99,9 @@ class SampleAttentionGraph:
         return self.out
 
     def check(self) -> None:
-        """Raise InputError if the last replay saw NaN/Inf in q/k/v (host sync)."""
-        if int(self.flag.item()) != 0:
-            raise InputError("q/k/v contain NaN or Inf")
+        """Raise InputError if the last replay saw NaN/Inf in q/k/v, or the
+        reference's stage-3 errors from the device status word (host sync)."""
+        raise_on_flags(self.flag, self.batch.q.device)
 
     def n_rescored(self) -> int:
         return self.selection.n_rescored()

@@ -17,9 +17,10 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import InputError
+from .errors import InputError, InternalInvariantError
 
-__all__ = ["AttentionHead", "HeadSet", "HeadBatch", "check_finite", "check_finite_async"]
+__all__ = ["AttentionHead", "HeadSet", "HeadBatch", "check_finite", "check_finite_async", "check_status", "dcall",
+           "raise_on_flags"]
 
 _DTYPES = {torch.bfloat16: _lib.SA_BF16, torch.float32: _lib.SA_FP32}
 
@@ -87,6 +88,16 @@ class HeadSet:
         return iter(self.heads)
 
 
+def dcall(device: torch.device, name: str, *args) -> int:
+    """_lib.call with `device` current: kernels launch on the device that owns
+    the tensors (and the per-device shared-memory opt-ins apply to it), whatever
+    the caller's current device is."""
+    if device.index is not None and device.index != torch.cuda.current_device():
+        with torch.cuda.device(device):
+            return _lib.call(name, *args)
+    return _lib.call(name, *args)
+
+
 def _stream(t: torch.Tensor) -> int:
     return torch.cuda.current_stream(t.device).cuda_stream
 
@@ -95,7 +106,7 @@ def check_finite_async(tensors, flag: torch.Tensor, stream: int) -> None:
     """Queue the NaN/Inf scan of `tensors` on `stream`, OR-ing into the int32
     device flag; the caller reads the flag later (no synchronisation here)."""
     for t in tensors:
-        _lib.call("sa_check_finite", t.data_ptr(), _DTYPES[t.dtype], t.numel(), flag.data_ptr(), stream)
+        dcall(t.device, "sa_check_finite", t.data_ptr(), _DTYPES[t.dtype], t.numel(), flag.data_ptr(), stream)
 
 
 def check_finite(*tensors: torch.Tensor) -> None:
@@ -104,9 +115,49 @@ def check_finite(*tensors: torch.Tensor) -> None:
     dev = tensors[0].device
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     for t in tensors:
-        _lib.call("sa_check_finite", t.data_ptr(), _DTYPES[t.dtype], t.numel(), flag.data_ptr(), _stream(t))
+        dcall(t.device, "sa_check_finite", t.data_ptr(), _DTYPES[t.dtype], t.numel(), flag.data_ptr(), _stream(t))
     if int(flag.item()) != 0:
         raise InputError("q/k/v contain NaN or Inf")
+
+
+def _read_status(device: torch.device) -> list:
+    import ctypes
+
+    buf = (ctypes.c_uint * 4)()
+    with torch.cuda.device(device):
+        _lib.call("sa_status", buf, 1)
+    return list(buf)
+
+
+def check_status(device: torch.device) -> None:
+    """Read (and reset) the device status word the stage-3 kernels fill
+    (sa_status; synchronises the device) and raise the reference's exception
+    for the first violation: InputError for a query block without active key
+    blocks (ref executor.py:131-132), InternalInvariantError for a mask that
+    breaks the BlockMask invariants (filtering.py:97-106) or an empty softmax
+    normaliser (executor.py:150-153)."""
+    bits, h, qb, n = _read_status(device)
+    if not bits:
+        return
+    where = f"head {h} query block {qb}" + (f" (and {n - 1} more)" if n > 1 else "")
+    if bits & _lib.SA_STATUS_EMPTY_BLOCK:
+        raise InputError(f"query block {qb} has no active key blocks ({where})")
+    if bits & _lib.SA_STATUS_MASK:
+        raise InternalInvariantError(f"block mask violates its invariants (kb <= qb, ascending, diagonal kept) "
+                                     f"at {where}")
+    raise InternalInvariantError(f"query block {qb} produced an empty softmax normalizer ({where})")
+
+
+def raise_on_flags(finite_flag: torch.Tensor | None, device: torch.device) -> None:
+    """One host sync for everything a call checked on the device: the NaN/Inf
+    flag of its inputs (InputError, core.py:30-37) first, then the stage-3
+    status word (a non-finite input also poisons the normaliser, so the input
+    error wins and the status is cleared)."""
+    bad_input = finite_flag is not None and int(finite_flag.item()) != 0
+    if bad_input:
+        _read_status(device)
+        raise InputError("q/k/v contain NaN or Inf")
+    check_status(device)
 
 
 @dataclass
@@ -121,6 +172,7 @@ class HeadBatch:
     v: torch.Tensor
     group: int = 1
     q_head0: int = 0
+    head_ids: tuple | None = None  # reference head ids (AttentionHead.head_id) when built from heads
 
     def __post_init__(self):
         q, k, v = self.q, self.k, self.v
@@ -190,4 +242,5 @@ class HeadBatch:
                 parts.append(t.to(device=device, dtype=dtype))
             return torch.stack(parts).contiguous()
 
-        return cls(stack("q"), stack("k"), stack("v"), group=1, q_head0=0)
+        return cls(stack("q"), stack("k"), stack("v"), group=1, q_head0=0,
+                   head_ids=tuple(int(h.head_id) for h in heads))

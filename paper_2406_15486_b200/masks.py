@@ -17,6 +17,7 @@ import torch
 
 from . import _lib
 from .errors import InputError
+from .heads import dcall
 
 __all__ = ["ChunkSelection", "SelectedIndices", "BlockMask"]
 
@@ -259,8 +260,8 @@ class BlockMask:
         nb = -(-S // blk)
         cnt = torch.empty((n_heads, nb), dtype=torch.int32, device=device)
         idx = torch.empty((n_heads, _tri(nb)), dtype=torch.int32, device=device)
-        _lib.call("sa_full_mask", n_heads, nb, cnt.data_ptr(), idx.data_ptr(),
-                  torch.cuda.current_stream(device).cuda_stream)
+        dcall(device, "sa_full_mask", n_heads, nb, cnt.data_ptr(), idx.data_ptr(),
+              torch.cuda.current_stream(device).cuda_stream)
         return cls(blk, S, cnt, idx)
 
     # ------------------------------------------------------------ scheduling
@@ -274,7 +275,7 @@ class BlockMask:
             if n < 0:
                 raise InputError(f"bad schedule geometry (heads {self.n_heads}, group {group}, q_head0 {q_head0})")
             order = torch.empty(n, dtype=torch.int32, device=self.device)
-            _lib.call("sa_schedule", self.kv_cnt.data_ptr(), self.n_heads, nb, group, q_head0, order.data_ptr(),
-                      torch.cuda.current_stream(self.device).cuda_stream)
+            dcall(self.device, "sa_schedule", self.kv_cnt.data_ptr(), self.n_heads, nb, group, q_head0,
+                  order.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
             self._order = (key, order)
         return self._order[1]

@@ -54,59 +54,72 @@ def shard_heads(Hq: int, Hkv: int, world: int, rank: int) -> HeadShard:
 
 def sample_attention_sharded(q_local: torch.Tensor, k_local: torch.Tensor, v_local: torch.Tensor,
                              shard: HeadShard, heads_per_chunk: int = 1, gather: bool = True,
-                             process_group=None, compute_fn=None, **kw):
-    """Run this rank's heads in chunks; after each chunk, all-gather its output
-    (on a side stream for CUDA tensors, so the NVLink transfer overlaps the
-    next chunk's compute).
+                             process_group=None, compute_fn=None, out: torch.Tensor | None = None, **kw):
+    """Run this rank's heads in chunks of `heads_per_chunk`.  With gather, the
+    job's output [Hq,S,d] is allocated once and this rank computes straight
+    into its own head rows; after each chunk every rank's rows of that chunk
+    are broadcast in place from their owner (one NCCL broadcast per rank, on a
+    side stream for CUDA tensors, so the NVLink transfer overlaps the next
+    chunk's compute).  No temporaries, no copies: a head's rows are a
+    contiguous slice of the final buffer.  Nothing synchronises the host.
 
     compute_fn(q, k, v, q_head0=, group=, out=, **kw) defaults to
-    sample_attention; the CPU multi-process tests inject the oracle here.
-    Returns (local_out [H_local,S,d], gathered [Hq,S,d] or None)."""
+    sample_attention with check_inputs=False (no host sync per chunk); the CPU
+    multi-process tests inject the oracle here.
+    Returns (local_out [H_local,S,d], gathered [Hq,S,d] or None); local_out is
+    a view of gathered when gathering."""
     import torch.distributed as dist
 
     if compute_fn is None:
-        from .pipeline import sample_attention as compute_fn
+        from .pipeline import sample_attention
+
+        def compute_fn(*a, **k2):
+            k2.setdefault("check_inputs", False)
+            return sample_attention(*a, **k2)
     H, S, d = q_local.shape
     if H != len(shard.q_heads):
         raise InputError(f"shard owns {len(shard.q_heads)} heads, got {H}")
-    out = torch.empty_like(q_local)
     world = shard.world
     do_gather = gather and world > 1
+    if do_gather:
+        full = out if out is not None else torch.empty((world * H, S, d), dtype=q_local.dtype,
+                                                       device=q_local.device)
+        if tuple(full.shape) != (world * H, S, d) or not full.is_contiguous():
+            raise InputError(f"out must be a contiguous [{world * H},{S},{d}] tensor")
+        mine = full[shard.rank * H:(shard.rank + 1) * H]
+    else:
+        full = None
+        mine = out if out is not None else torch.empty_like(q_local)
     on_gpu = q_local.is_cuda
     comm = torch.cuda.Stream(device=q_local.device) if (do_gather and on_gpu) else None
     main = torch.cuda.current_stream(q_local.device) if on_gpu else None
-    pending = []
+    works = []
     for h0 in range(0, H, heads_per_chunk):
         h1 = min(H, h0 + heads_per_chunk)
         g0 = shard.q_heads[h0]
         kv0 = shard.local_kv(g0)
         kv1 = shard.local_kv(shard.q_heads[h1 - 1]) + 1
         compute_fn(q_local[h0:h1], k_local[kv0:kv1], v_local[kv0:kv1], q_head0=g0, group=shard.group,
-                   out=out[h0:h1], **kw)
+                   out=mine[h0:h1], **kw)
         if not do_gather:
             continue
-        parts = [torch.empty_like(out[h0:h1]) for _ in range(world)]
         if comm is not None:
             ev = torch.cuda.Event()
             ev.record(main)
             comm.wait_event(ev)
-            with torch.cuda.stream(comm):
-                work = dist.all_gather(parts, out[h0:h1], group=process_group, async_op=True)
-        else:
-            work = dist.all_gather(parts, out[h0:h1], group=process_group, async_op=True)
-        pending.append((h0, h1, work, parts))
+        with (torch.cuda.stream(comm) if comm is not None else _null()):
+            for r in range(world):
+                works.append(dist.broadcast(full[r * H + h0:r * H + h1], src=r, group=process_group,
+                                            async_op=True))
     if not do_gather:
-        return out, None
-    gathered = torch.empty((world, H, S, d), dtype=q_local.dtype, device=q_local.device)
-    ctx = torch.cuda.stream(comm) if comm is not None else _null()
-    with ctx:
-        for h0, h1, work, parts in pending:
-            work.wait()
-            for r, p in enumerate(parts):
-                gathered[r, h0:h1].copy_(p)
+        return mine, None
+    with (torch.cuda.stream(comm) if comm is not None else _null()):
+        for w in works:
+            w.wait()
     if comm is not None:
         main.wait_stream(comm)
-    return out, gathered.reshape(world * H, S, d)
+        full.record_stream(comm)
+    return mine, full
 
 
 class _null:

@@ -19,7 +19,7 @@ import torch
 
 from .config import ChunkPlan, SparseConfig, n_blocks, plan_chunks, resolve_config
 from .errors import InputError
-from .heads import HeadBatch, HeadSet, check_finite
+from .heads import HeadBatch, HeadSet, check_finite_async, check_status, raise_on_flags
 from .masks import BlockMask
 from .stages import (FlopReport, block_reduce, flop_accounting, merge_index, sample_scores, select,
                      sparse_attention)
@@ -64,10 +64,17 @@ def sample_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, alpha: f
     alpha: CRA threshold (alpha_c = alpha_s = alpha unless given);
     sample_ratio / chunk_n: how many 128-row query windows stage 1 scores;
     sink_blocks / local_blocks: optional forced key blocks (defaults reproduce
-    the reference, which forces only the diagonal).  Returns (out, result)."""
+    the reference, which forces only the diagonal).  Returns (out, result).
+
+    check_inputs: scan q/k/v for NaN/Inf (InputError, ref core.py:30-37) and
+    read the stage-3 invariant status (ref executor.py:131-132, 150-153); both
+    are device flags read with ONE host sync after every stage is enqueued.
+    check_inputs=False leaves the call free of host synchronisation."""
     batch = HeadBatch.from_tensors(q, k, v, group=group, q_head0=q_head0)
+    flag = None
     if check_inputs:
-        check_finite(batch.q, batch.k, batch.v)
+        flag = torch.zeros(1, dtype=torch.int32, device=batch.q.device)
+        check_finite_async((batch.q, batch.k, batch.v), flag, batch.stream)
     cfg = resolve_config(batch.S, alpha, alpha_c, alpha_s, chunk_n, sample_ratio, blk)
     plan = plan_chunks(batch.S, cfg)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings else None
@@ -85,6 +92,8 @@ def sample_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, alpha: f
     o, _ = sparse_attention(batch, mask, out=out, lse=lse, report=False)
     if ev:
         ev[3].record()
+    if check_inputs:
+        raise_on_flags(flag, batch.q.device)
     return o, SampleAttentionResult(cfg, plan, mask, sel.flags, ev, lse)
 
 
@@ -213,7 +222,8 @@ def run_pipeline(head_set, cfg: SparseConfig, want_oracle: bool = False, seed: i
     S, d, H = batch.S, batch.d, batch.Hq
     if want_oracle and S > ORACLE_CAP:
         raise InputError(f"oracle metrics need S <= {ORACLE_CAP}, got {S}; run without --oracle")
-    check_finite(batch.q, batch.k, batch.v)
+    flag = torch.zeros(1, dtype=torch.int32, device=batch.q.device)
+    check_finite_async((batch.q, batch.k, batch.v), flag, batch.stream)
     plan = plan_chunks(S, cfg)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     ev[0].record()
@@ -222,9 +232,10 @@ def run_pipeline(head_set, cfg: SparseConfig, want_oracle: bool = False, seed: i
     sel = select(reduced, cfg, guard=guard)
     mask = merge_index(sel, plan, cfg.blk, S)
     ev[2].record()
-    out, flop = sparse_attention(batch, mask)
+    out, flop = sparse_attention(batch, mask, check=False)
     ev[3].record()
-    torch.cuda.synchronize(batch.q.device)
+    raise_on_flags(flag, batch.q.device)
+    flop.wall_time_sparse = ev[2].elapsed_time(ev[3]) / 1e3
     t_s, t_f, t_x = (ev[i].elapsed_time(ev[i + 1]) / 1e3 / H for i in range(3))
     dense = torch.from_numpy(mask.to_dense()).to(batch.q.device)  # [H, nb, nb]
     kv_of = [(batch.q_head0 + h) // batch.group - batch.q_head0 // batch.group for h in range(H)]
@@ -248,7 +259,7 @@ def run_pipeline(head_set, cfg: SparseConfig, want_oracle: bool = False, seed: i
         kh = batch.k[kv_of[h]]
         kept = torch.cat([_retained(_causal_probs(batch.q[h, r], kh, r), r, dense[h], blk) for r in rows_all])
         hm = HeadMetrics(
-            head_id=h,
+            head_id=batch.head_ids[h] if batch.head_ids else batch.q_head0 + h,
             cra_sampled_min=float(kept.min()), cra_sampled_mean=float(kept.mean()),
             block_density=float(flop.per_head_active[h]) / mask.causal_count(),
             sparsity_ratio=1.0 - float(entries[h]) / total_causal,

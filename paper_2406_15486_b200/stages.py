@@ -29,7 +29,7 @@ import torch
 from . import _lib
 from .config import ChunkPlan, SparseConfig, n_blocks
 from .errors import InputError
-from .heads import AttentionHead, HeadBatch, HeadSet
+from .heads import AttentionHead, HeadBatch, HeadSet, check_status, dcall
 from .masks import BlockMask, SelectedIndices, _tri
 
 __all__ = [
@@ -154,7 +154,7 @@ class ReducedScores:
 
 def _stage1(b: HeadBatch, plan: ChunkPlan, col, slash, mode: int, only=None) -> None:
     ws = _workspace(b, plan.blk, plan.chunk_n)
-    _lib.call("sa_stage1", b.q.data_ptr(), b.k.data_ptr(), b.dtype_code, b.S, b.Hq, b.Hkv, b.d, plan.blk,
+    dcall(b.q.device, "sa_stage1", b.q.data_ptr(), b.k.data_ptr(), b.dtype_code, b.S, b.Hq, b.Hkv, b.d, plan.blk,
               b.group, b.q_head0, plan.chunk_n, plan.itv, col.data_ptr(), slash.data_ptr(), mode,
               None if only is None else only.data_ptr(), ws.data_ptr(), ws.numel(), b.stream)
 
@@ -190,7 +190,7 @@ def _vector_select(scores, alpha, k=None):
     k_in = None
     if k is not None:
         k_in = torch.tensor([[[k, k]]], dtype=torch.int32, device=dev)
-    _lib.call("sa_select", t.data_ptr(), t.data_ptr(), 1, 1, s.size, alpha, alpha, 0.0, None, None,
+    dcall(dev, "sa_select", t.data_ptr(), t.data_ptr(), 1, 1, s.size, alpha, alpha, 0.0, None, None,
               None if k_in is None else k_in.data_ptr(), k_out.data_ptr(), idx.data_ptr(),
               torch.cuda.current_stream(dev).cuda_stream)
     kk = int(k_out[0, 0, 0].item())
@@ -252,12 +252,12 @@ def select(reduced: ReducedScores, cfg: SparseConfig, guard: str = "auto",
     idx_sel = torch.empty((H, cn, 2, nb), dtype=torch.int32, device=dev)
     use_guard = guard == "auto" and reduced.mode == "tensor"
     flags = torch.zeros(H * cn, dtype=torch.int32, device=dev) if use_guard else None
-    _lib.call("sa_select", reduced.col.data_ptr(), reduced.slash.data_ptr(), H, cn, nb, cfg.alpha_c,
+    dcall(dev, "sa_select", reduced.col.data_ptr(), reduced.slash.data_ptr(), H, cn, nb, cfg.alpha_c,
               cfg.alpha_s, guard_eps if use_guard else 0.0, None if flags is None else flags.data_ptr(),
               None, None, k_sel.data_ptr(), idx_sel.data_ptr(), st)
     if use_guard:
         _stage1(b, plan, reduced.col, reduced.slash, _lib.SA_STAGE1_EXACT, only=flags)
-        _lib.call("sa_select", reduced.col.data_ptr(), reduced.slash.data_ptr(), H, cn, nb, cfg.alpha_c,
+        dcall(dev, "sa_select", reduced.col.data_ptr(), reduced.slash.data_ptr(), H, cn, nb, cfg.alpha_c,
                   cfg.alpha_s, 0.0, None, flags.data_ptr(), None, k_sel.data_ptr(), idx_sel.data_ptr(), st)
     return Selection(k_sel, idx_sel, flags, guard)
 
@@ -300,7 +300,7 @@ def merge_index(selected, plan: ChunkPlan, blk: int, S: int, sink_blocks: int = 
     kv_idx = torch.empty((H, _tri(nb)), dtype=torch.int32, device=dev)
     ab = torch.empty(H, dtype=torch.int64, device=dev)
     ae = torch.empty(H, dtype=torch.int64, device=dev)
-    _lib.call("sa_merge", selected.k_sel.data_ptr(), selected.idx_sel.data_ptr(), H, plan.chunk_n, nb, S,
+    dcall(dev, "sa_merge", selected.k_sel.data_ptr(), selected.idx_sel.data_ptr(), H, plan.chunk_n, nb, S,
               blk, plan.itv, sink_blocks, local_blocks, kv_cnt.data_ptr(), kv_idx.data_ptr(), ab.data_ptr(),
               ae.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
     mask = BlockMask(blk, S, kv_cnt, kv_idx, selected.k_sel, selected.idx_sel, ab, ae)
@@ -363,13 +363,25 @@ def flop_accounting(mask: BlockMask, S: int, d: int) -> FlopReport:
     )
 
 
+def _check_buffer(name: str, t: torch.Tensor, shape: tuple, dtype, device) -> None:
+    if not isinstance(t, torch.Tensor) or tuple(t.shape) != tuple(shape) or t.dtype != dtype \
+            or t.device != device or not t.is_contiguous():
+        got = (tuple(t.shape), t.dtype, str(t.device), t.is_contiguous()) if isinstance(t, torch.Tensor) else type(t)
+        raise InputError(f"{name} must be a contiguous {dtype} tensor of shape {tuple(shape)} on {device}, got {got}")
+
+
 def sparse_attention(heads, mask: BlockMask, out: torch.Tensor | None = None,
-                     lse: torch.Tensor | None = None, report: bool = True):
+                     lse: torch.Tensor | None = None, report: bool = True, check: bool | None = None):
     """Block-sparse causal attention over the mask's active blocks
     (executor.py:104-158).  Returns (out [H, S, d] in the input dtype,
-    FlopReport with the kernel's touched-block count) — or (out, None) with
-    report=False, which keeps the call free of host synchronisation."""
+    FlopReport with the kernel's touched-block count and wall_time_sparse,
+    the kernel's CUDA-event time) — or (out, None) with report=False, which
+    keeps the call free of host synchronisation.  check (default: report)
+    reads the device status word and raises the reference's errors for an
+    empty query block / broken mask invariants / empty normaliser."""
     b = as_batch(heads)
+    if check is None:
+        check = report
     if mask.n_heads != b.Hq:
         raise InputError(f"mask covers {mask.n_heads} heads, batch has {b.Hq}")
     nb = n_blocks(b.S, mask.blk)
@@ -377,13 +389,25 @@ def sparse_attention(heads, mask: BlockMask, out: torch.Tensor | None = None,
         raise InputError(f"mask has {mask.n_qblocks} blocks of {mask.blk}, head needs {nb} for S={b.S}")
     if out is None:
         out = torch.empty_like(b.q)
+    else:
+        _check_buffer("out", out, b.q.shape, b.q.dtype, b.q.device)
+    if lse is not None:
+        _check_buffer("lse", lse, (b.Hq, b.S), torch.float32, b.q.device)
     touched = torch.zeros(b.Hq, dtype=torch.int64, device=b.q.device) if report else None
-    _lib.call("sa_sparse_forward", b.q.data_ptr(), b.k.data_ptr(), b.v.data_ptr(), b.dtype_code, b.S, b.Hq,
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if report else None
+    if ev:
+        ev[0].record()
+    dcall(b.q.device, "sa_sparse_forward", b.q.data_ptr(), b.k.data_ptr(), b.v.data_ptr(), b.dtype_code, b.S, b.Hq,
               b.Hkv, b.d, mask.blk, b.group, b.q_head0, mask.kv_cnt.data_ptr(), mask.kv_idx.data_ptr(),
               mask.order(b.group, b.q_head0).data_ptr(), out.data_ptr(), None if lse is None else lse.data_ptr(),
               None if touched is None else touched.data_ptr(), b.stream)
+    if ev:
+        ev[1].record()
+    if check:
+        check_status(b.q.device)
     if not report:
         return out, None
     rep = flop_accounting(mask, b.S, b.d)
     rep.active_blocks = int(touched.sum().item())
+    rep.wall_time_sparse = ev[0].elapsed_time(ev[1]) / 1e3
     return out, rep

@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from .errors import InputError
-from .heads import check_finite_async
+from .heads import check_finite_async, raise_on_flags
 from .pipeline import sample_attention
 
 __all__ = ["sample_attention_host"]
@@ -132,6 +132,8 @@ def sample_attention_host(q, k, v, heads_per_group: int = 4, device=None, out: t
     for t in (dq, dk, dv, dout, flag):
         t.record_stream(h2d)
         t.record_stream(d2h)
-    if check_inputs and int(flag.item()) != 0:
-        raise InputError("q/k/v contain NaN or Inf")
+    # `out` is host memory: the caller may read it as soon as we return
+    d2h.synchronize()
+    if check_inputs:
+        raise_on_flags(flag, dev)
     return out, results

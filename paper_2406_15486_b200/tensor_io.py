@@ -23,7 +23,7 @@ import torch
 
 from . import _lib
 from .errors import InputError
-from .heads import AttentionHead, HeadBatch, HeadSet
+from .heads import AttentionHead, HeadBatch, HeadSet, dcall
 
 __all__ = ["MAGIC", "load_tensors", "load_tensors_device", "save_tensors"]
 
@@ -117,8 +117,8 @@ def load_tensors_device(path, device=None, dtype=torch.bfloat16) -> HeadBatch:
         host = torch.from_numpy(np.asarray(mm[payload:]).view("<f4").reshape(n, 3, S, d))
     cube = host.to(dev)  # fp32, one H2D copy
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    _lib.call("sa_check_finite", cube.data_ptr(), _lib.SA_FP32, cube.numel(), flag.data_ptr(),
-              torch.cuda.current_stream(dev).cuda_stream)
+    dcall(cube.device, "sa_check_finite", cube.data_ptr(), _lib.SA_FP32, cube.numel(), flag.data_ptr(),
+          torch.cuda.current_stream(cube.device).cuda_stream)
     if int(flag.item()) != 0:  # diagnostics only: name the first bad element like the reference
         _first_bad(path, np.asarray(mm[payload:]).view("<f4"), payload)
         raise InputError(f"{path}: non-finite value in the payload")

@@ -215,7 +215,9 @@ def test_determinism(sa):
     o1, r1 = sa.sample_attention(qt, kt, vt, alpha=0.95, chunk_n=3)
     o2, r2 = sa.sample_attention(qt, kt, vt, alpha=0.95, chunk_n=3)
     assert torch.equal(o1, o2)
-    assert r1.mask.serialize() if r1.mask.n_heads == 1 else True
+    assert r1.mask.n_heads == 1
+    assert r1.mask.serialize() == r2.mask.serialize()
+    assert r1.mask.selections() == r2.mask.selections()
     assert torch.equal(r1.mask.kv_cnt, r2.mask.kv_cnt)
 
 
@@ -386,3 +388,79 @@ def test_cra_full_beyond_the_oracle_cap(sa):
     _, res = sa.sample_attention(q2, k2, v2, alpha=0.95, chunk_n=1)
     m16, a16 = sa.cra_full(sa.HeadBatch.from_tensors(q2, k2, v2), res.mask)
     assert 0.0 < m16[0] <= a16[0] <= 1.0 + 1e-12
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_device_invariant_errors(sa, dtype):
+    """The stage-3 kernels check the mask invariants the reference's BlockMask
+    enforces (filtering.py:97-106) and the executor's errors (executor.py:
+    131-132 InputError for a query block without active key blocks, 150-153
+    InternalInvariantError for an empty normaliser) on the device; the host
+    raises them from the status word, which is then clear for the next call."""
+    S, nb = 1024, 8
+    rng = np.random.default_rng(0)
+    q, k, v = (O_bf16(rng.standard_normal((S, 128))) for _ in range(3))
+    qt, kt, vt = to_dev((q, k, v), dtype)
+    batch = sa.HeadBatch.from_tensors(qt, kt, vt)
+    grid = np.tril(np.ones((nb, nb), dtype=bool))
+
+    def fresh():
+        return sa.BlockMask.from_dense(128, grid, S=S, device="cuda")
+
+    out, _ = sa.sparse_attention(batch, fresh())  # valid: no error
+    m = fresh()
+    m.kv_cnt[0, 3] = 0  # query block 3 without any key block
+    with pytest.raises(sa.InputError, match="no active key blocks"):
+        sa.sparse_attention(batch, m)
+    m = fresh()
+    m.kv_cnt[0, 5] = 5  # list 0..4: the diagonal is missing
+    with pytest.raises(sa.InternalInvariantError, match="invariants"):
+        sa.sparse_attention(batch, m)
+    m = fresh()
+    m.kv_idx[0, 3 + 1] = 3  # query block 2 lists [0, 3, 2]: kb > qb and unsorted
+    with pytest.raises(sa.InternalInvariantError, match="invariants"):
+        sa.sparse_attention(batch, m)
+    bad = qt.clone()
+    bad[0, 200, 5] = float("nan")
+    with pytest.raises(sa.InternalInvariantError, match="normalizer"):
+        sa.sparse_attention(sa.HeadBatch.from_tensors(bad, kt, vt), fresh())
+    with pytest.raises(sa.InputError, match="NaN"):  # the input check wins over the normaliser
+        sa.sample_attention(bad, kt, vt, alpha=0.95, chunk_n=2)
+    out2, _ = sa.sparse_attention(batch, fresh())  # status was reset
+    assert torch.equal(out, out2)
+
+
+def test_out_buffer_validation(sa):
+    qt, kt, vt = to_dev([O_bf16(np.random.default_rng(1).standard_normal((512, 128)))] * 3, torch.bfloat16)
+    with pytest.raises(sa.InputError, match="out must be"):
+        sa.sample_attention(qt, kt, vt, out=torch.empty(qt.shape, dtype=torch.float32, device="cuda"))
+    with pytest.raises(sa.InputError, match="out must be"):
+        sa.sample_attention(qt, kt, vt, out=torch.empty((1, 256, 128), dtype=torch.bfloat16, device="cuda"))
+
+
+@pytest.mark.parametrize("seed,scale,sink", [(0, 2.0, 30.0), (1, 3.0, 60.0), (2, 2.5, 120.0), (3, 4.0, 0.0)])
+def test_guard_auto_matches_always_at_large_logits(sa, seed, scale, sink):
+    """High-magnitude logits (q, k scaled so q.k/sqrt(d) has std scale^2, plus
+    attention-sink keys with logits up to `sink`): the tensor-core stage-1
+    error grows with the logit magnitude, so the guard margin scales with a
+    per-(head, chunk) logit bound; guard='auto' must select exactly what the
+    all-fp64 guard='always' selects, which must equal the oracle's."""
+    S, cn = 4096, 4
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((S, 128)) * scale
+    k = rng.standard_normal((S, 128)) * scale
+    v = rng.standard_normal((S, 128))
+    if sink:
+        u = rng.standard_normal(128)
+        u /= np.linalg.norm(u)
+        q += np.outer(np.full(S, 1.0), u) * np.sqrt(sink)
+        pos = rng.choice(S, size=24, replace=False)
+        k[pos] += np.outer(rng.uniform(0.3, 1.0, size=24), u) * np.sqrt(sink) * np.sqrt(128)
+    q, k, v = (O_bf16(a) for a in (q, k, v))
+    qt, kt, vt = to_dev((q, k, v), torch.bfloat16)
+    for alpha in (0.9, 0.95, 0.98):
+        _, ra = sa.sample_attention(qt, kt, vt, alpha=alpha, chunk_n=cn, guard="auto")
+        _, rw = sa.sample_attention(qt, kt, vt, alpha=alpha, chunk_n=cn, guard="always")
+        assert ra.mask.selections() == rw.mask.selections(), (alpha, ra.n_rescored())
+        ref = O.run_head(q, k, None, alpha, alpha, cn, 128, with_output=False)
+        assert [(c.i_c, c.i_s) for c in rw.mask.selections()[0].chunks] == ref["selection"], alpha

@@ -40,7 +40,7 @@ def run():
 
 
 run()
-reader = lib.sa_debug_k3p2_profile if os.environ.get("SA_K3_IMPL", "").startswith("p") else lib.sa_debug_k3s_profile
+reader = lib.sa_debug_k3s_profile
 reader(buf, 1)
 run()
 reader(buf, 1)
@@ -50,10 +50,8 @@ names = {0: "softmax: wait S", 1: "softmax: pass 1 (max)", 2: "softmax: rescale"
          4: "softmax: wait O (epilogue)", 5: "mma: wait P part", 6: "mma: wait P full", 7: "mma: wait V",
          8: "mma: wait K", 9: "mma: wait Q", 10: "tma: wait K slot", 11: "tma: wait V slot",
          12: "mma: loop total"}
-print(f"{a.config} {'dense' if a.dense else 'sparse'}: {blocks} (item, block) pairs "
-      f"(pair kernel: union steps, per SM pair)")
+print(f"{a.config} {'dense' if a.dense else 'sparse'}: {blocks} (item, block) pairs")
 for i, nm in names.items():
     # softmax slots are summed over 4 warps of a tile (lane 0 each); others once per CTA
-    pair = os.environ.get("SA_K3_IMPL", "").startswith("p")
-    div = blocks * ((8 if pair else 4) if i <= 4 else 1)
+    div = blocks * (4 if i <= 4 else 1)
     print(f"{nm:28s} {c[i] / div:10.1f} cycles per (item, block)")
