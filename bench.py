@@ -458,6 +458,20 @@ def dense_rows(sa, q, k, v, group, flops, flush):
         rows["cudnn_sdpa"] = {"ms": round(ms, 3), "tflops": round(flops / ms / 1e9, 1)}
     except Exception as e:  # pragma: no cover - depends on the box
         rows["cudnn_sdpa"] = {"error": str(e)[:200]}
+    try:  # FlashAttention-4 (CuTe DSL, sm100 tcgen05 kernel) as shipped in vllm
+        from vllm.vllm_flash_attn.cute.interface import flash_attn_func as fa4
+
+        qf, kf, vf = (t.transpose(0, 1).contiguous()[None] for t in (q, k, v))  # [1, S, H, d]
+        res = fa4(qf, kf, vf, causal=True)
+        o4 = res[0] if isinstance(res, tuple) else res
+        ref = torch.nn.functional.scaled_dot_product_attention(q[None, :1], k[None, :1], v[None, :1], is_causal=True)
+        err = float((o4[0, :, 0].float() - ref[0, 0].float()).abs().max())
+        ms = timeit(lambda: fa4(qf, kf, vf, causal=True))
+        rows["flash_attn4_sm100"] = {"ms": round(ms, 3), "tflops": round(flops / ms / 1e9, 1),
+                                     "max_abs_err_head0_vs_sdpa": round(err, 5)}
+        del qf, kf, vf, o4, res
+    except Exception as e:  # pragma: no cover - depends on the box
+        rows["flash_attn4_sm100"] = {"error": str(e)[:200]}
     try:
         from flash_attn import flash_attn_func
 
@@ -553,8 +567,12 @@ def run_reference(args, rank, S, Hq, Hkv, d, alpha, chunk_n, workload):
 
     from paper_2406_15486_b200 import synth
 
-    q, k, v, kv = synth.make_inputs(S, Hq, Hkv, d, seed=args.seed, heads=[0], device="cpu")
-    qh, kh, vh = (t[0].double().numpy() for t in (q, k, v))
+    # the same bits our arm times: the seeded generator runs where our arm runs it (input plumbing,
+    # untimed); the reference algorithm itself only ever runs on the host
+    gen_dev = "cuda" if torch.cuda.is_available() else "cpu"
+    q, k, v, kv = synth.make_inputs(S, Hq, Hkv, d, seed=args.seed, heads=[0], device=gen_dev)
+    qh, kh, vh = (t[0].double().cpu().numpy() for t in (q, k, v))
+    del q, k, v
     runs = []
     for i in range(args.warmup + args.steps):
         r = cpu_sample(qh, kh, vh, alpha, chunk_n)

@@ -90,23 +90,29 @@ int sa_check_finite(const void* x, int dtype, int64_t n, int* flag_dev, void* st
  * Writes col/slash [Hq][cn][nb] fp64.  mode: SA_STAGE1_TENSOR or
  * SA_STAGE1_EXACT.  When only_flags != NULL, only (h, c) pairs with
  * only_flags[h*cn + c] != 0 are (re)computed (the exact re-score of pairs
- * sa_select flagged as too close to call). */
+ * sa_select flagged as too close to call).  logit_bound (optional, tensor mode,
+ * full calls only): [Hq][cn] doubles, max ||q_r|| * max ||k_j|| / sqrt(d) over
+ * the pair's sampled rows and the KV head's keys -- the scale of the
+ * tensor-core score error, which widens sa_select's guard margin. */
 int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, int d, int blk,
               int group, int q_head0, int chunk_n, int itv, double* col, double* slash,
-              int mode, const int* only_flags, void* workspace, size_t workspace_bytes,
-              void* stream);
+              double* logit_bound, int mode, const int* only_flags, void* workspace,
+              size_t workspace_bytes, void* stream);
 
 /* Stage 2a — replaces find_k + arg_topk per (head, chunk, direction)
  * (filtering.py:30-62, applied as in select_and_merge :245-255).
  * margin_eps > 0 enables the selection guard: flags[h*cn + c] is set to 1
  * when the alpha cut or the boundary tie gap lies within margin_eps * total
  * of a decision, i.e. when scores carrying that relative error could change
- * the reference's answer.  With only_flags != NULL only flagged pairs are
+ * the reference's answer; with logit_bound (sa_stage1's) the margin of pair
+ * hc is margin_eps * max(1, logit_bound[hc] / bound_ref) * total.  With
+ * only_flags != NULL only flagged pairs are
  * recomputed.  k_in != NULL ([Hq][cn][2]) skips find_k and takes the given k
  * (the reference's arg_topk(scores, k), filtering.py:51-62). */
 int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int nb,
-              double alpha_c, double alpha_s, double margin_eps, int* flags,
-              const int* only_flags, const int* k_in, int* k_out, int* idx_out, void* stream);
+              double alpha_c, double alpha_s, double margin_eps, const double* logit_bound,
+              double bound_ref, int* flags, const int* only_flags, const int* k_in, int* k_out,
+              int* idx_out, void* stream);
 
 /* Stage 2b — replaces merge_index (filtering.py:198-230): extends every
  * chunk's picks over its query region, unions straddling blocks, forces the

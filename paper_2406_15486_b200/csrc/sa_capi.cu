@@ -21,8 +21,8 @@
 namespace sa {
 
 int launch_select(const double* col, const double* slash, int Hq, int cn, int nb, double ac,
-                  double as, double eps, int* flags, const int* only, const int* k_in, int* k_out,
-                  int* idx_out, cudaStream_t st);
+                  double as, double eps, const double* bound, double bound_ref, int* flags, const int* only,
+                  const int* k_in, int* k_out, int* idx_out, cudaStream_t st);
 int launch_merge(const int* k_sel, const int* idx_sel, int Hq, int cn, int nb, int S, int blk,
                  int itv, int sink_blocks, int local_blocks, int* kv_cnt, int* kv_idx,
                  long long* ab, long long* ae, cudaStream_t st);
@@ -107,7 +107,6 @@ bool make_tmap_bf16_hsd(CUtensorMap* map, const void* base, int H, int S, int d,
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int dtype) {
-  (void)Hkv;
   (void)d;
   Workspace L{};
   const int nb = ceil_div(S, blk);
@@ -123,6 +122,8 @@ Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int d
   off = align_up(off + (size_t)Hq * cn * nb * 4 * sizeof(double));
   L.flag_list = off;
   off = align_up(off + (size_t)(Hq * cn + 2) * sizeof(int));
+  L.kmax2 = off;
+  off = align_up(off + (size_t)Hkv * sizeof(unsigned));
   L.total = off;
   return L;
 }
@@ -182,8 +183,9 @@ int sa_check_finite(const void* x, int dtype, int64_t n, int* flag_dev, void* st
 }
 
 int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, int d, int blk,
-              int group, int q_head0, int chunk_n, int itv, double* col, double* slash, int mode,
-              const int* only_flags, void* workspace, size_t workspace_bytes, void* stream) {
+              int group, int q_head0, int chunk_n, int itv, double* col, double* slash,
+              double* logit_bound, int mode, const int* only_flags, void* workspace,
+              size_t workspace_bytes, void* stream) {
   if (int e = check_geom(S, Hq, Hkv, d, blk, group, q_head0, dtype)) return e;
   if (!q || !k || !col || !slash || !workspace) return fail(SA_ERR_INVALID, "sa_stage1: null pointer");
   if (chunk_n < 1 || itv < 1) return fail(SA_ERR_INVALID, "sa_stage1: chunk_n and itv must be >= 1");
@@ -198,6 +200,8 @@ int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, i
   char* ws = static_cast<char*>(workspace);
   if (mode == SA_STAGE1_TENSOR) {
     if (dtype != SA_BF16) return fail(SA_ERR_UNSUPPORTED, "tensor-core stage 1 needs bf16 inputs");
+    if (logit_bound && !only_flags)
+      if (int e = launch_logit_bound(g, q, k, ws, L, logit_bound, st)) return e;
     return launch_stage1_tc(g, q, k, only_flags, ws, L, col, slash, st);
   }
   if (mode == SA_STAGE1_EXACT)
@@ -206,8 +210,8 @@ int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, i
 }
 
 int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int nb, double alpha_c,
-              double alpha_s, double margin_eps, int* flags, const int* only_flags, const int* k_in,
-              int* k_out, int* idx_out, void* stream) {
+              double alpha_s, double margin_eps, const double* logit_bound, double bound_ref, int* flags,
+              const int* only_flags, const int* k_in, int* k_out, int* idx_out, void* stream) {
   if (!(alpha_c >= 0.0 && alpha_c <= 1.0))
     return fail(SA_ERR_INVALID, "alpha_c must be in [0, 1]");
   if (!(alpha_s >= 0.0 && alpha_s <= 1.0))
@@ -215,7 +219,9 @@ int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int n
   if (Hq < 1 || chunk_n < 1 || nb < 1) return fail(SA_ERR_INVALID, "sa_select: empty geometry");
   if (!col || !slash || !k_out || !idx_out) return fail(SA_ERR_INVALID, "sa_select: null pointer");
   if (margin_eps > 0.0 && !flags) return fail(SA_ERR_INVALID, "sa_select: guard needs flags");
-  return launch_select(col, slash, Hq, chunk_n, nb, alpha_c, alpha_s, margin_eps, flags, only_flags,
+  if (logit_bound && !(bound_ref > 0.0)) return fail(SA_ERR_INVALID, "sa_select: bound_ref must be > 0");
+  return launch_select(col, slash, Hq, chunk_n, nb, alpha_c, alpha_s, margin_eps, logit_bound, bound_ref, flags,
+                       only_flags,
                        k_in, k_out, idx_out, static_cast<cudaStream_t>(stream));
 }
 

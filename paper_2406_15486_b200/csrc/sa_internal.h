@@ -52,6 +52,7 @@ struct Workspace {
   size_t x_part;    // double [3][Hq*cn*blk*nb]   exact (A, B, m) per (row, key block)
   size_t part3;     // double [Hq*cn*nb][4]       (col, slash X-1, X, X+1) per key block
   size_t flag_list; // int    [Hq*cn + 2]             compacted guard-flagged pairs: count, then indices
+  size_t kmax2;     // uint   [Hkv]                 max ||k_j||^2 per KV head (guard logit bound)
   size_t total;
 };
 Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int dtype);
@@ -60,6 +61,9 @@ Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int d
 int launch_stage1_exact(const Stage1Geom& g, const void* q, const void* k, int dtype,
                         const int* only_flags, char* ws, const Workspace& L, double* col,
                         double* slash, cudaStream_t st);
+// Guard logit bound per (head, chunk): max ||q_r|| * max ||k_j|| / sqrt(d) (bf16 inputs).
+int launch_logit_bound(const Stage1Geom& g, const void* q, const void* k, char* ws, const Workspace& L,
+                       double* bound, cudaStream_t st);
 int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const int* only_flags,
                      char* ws, const Workspace& L, double* col, double* slash, cudaStream_t st);
 // rows' global max / sum, fold into part3, scatter into col / slash.  With

@@ -224,7 +224,78 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+// ---- selection-guard logit bound.  The tensor-core scores carry the fp32
+// accumulation error of q.k, which grows with sum_i |q_i k_i| <= ||q|| ||k||;
+// the guard margin of a (head, chunk) is scaled by
+//   bound = max_{sampled rows r} ||q_r|| * max_{keys j} ||k_j|| / sqrt(d)
+// (Cauchy-Schwarz), so large-logit heads get a proportionally wider margin.
+// One warp per key row: max ||k_j||^2 per KV head (nonnegative floats order
+// like their bit patterns, so atomicMax on the bits is a float max).
+__global__ void k_key_norm(const __nv_bfloat16* __restrict__ k, int S, unsigned* __restrict__ kmax2) {
+  const int kvh = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  float best = 0.f;
+  for (int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < S; j += gridDim.x * (blockDim.x >> 5)) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(k + ((size_t)kvh * S + j) * 128) + lane);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    float ss = a.x * a.x + a.y * a.y + b.x * b.x + b.y * b.y;
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    best = fmaxf(best, ss);
+  }
+  __shared__ float s_best[32];
+  if (lane == 0) s_best[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = fmaxf(best, s_best[w]);
+    atomicMax(kmax2 + kvh, __float_as_uint(best));
+  }
+}
+
+// One CTA per (head, chunk); thread r = sampled row r of the window.
+__global__ void k_pair_bound(const __nv_bfloat16* __restrict__ q, Stage1Geom g, const unsigned* __restrict__ kmax2,
+                             double* __restrict__ bound) {
+  const int hc = blockIdx.x, h = hc / g.cn, c = hc - h * g.cn;
+  const int se = min(g.S, (c + 1) * g.itv), ss = max(0, se - g.blk);
+  float qq = 0.f;
+  for (int r = ss + (int)threadIdx.x; r < se; r += blockDim.x) {
+    const uint4* row = reinterpret_cast<const uint4*>(q + ((size_t)h * g.S + r) * 128);
+    float acc = 0.f;
+#pragma unroll 4
+    for (int t = 0; t < 16; ++t) {
+      const uint4 u = __ldg(row + t);
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+        acc = fmaf(f.x, f.x, fmaf(f.y, f.y, acc));
+      }
+    }
+    qq = fmaxf(qq, acc);
+  }
+  for (int o = 16; o > 0; o >>= 1) qq = fmaxf(qq, __shfl_xor_sync(0xffffffffu, qq, o));
+  __shared__ float s_q[32];
+  if ((threadIdx.x & 31) == 0) s_q[threadIdx.x >> 5] = qq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) qq = fmaxf(qq, s_q[w]);
+    const float kk = __uint_as_float(kmax2[kv_head_of(h, g.group, g.q_head0)]);
+    bound[hc] = sqrt((double)qq * (double)kk) / sqrt((double)g.d);
+  }
+}
+
 }  // namespace
+
+int launch_logit_bound(const Stage1Geom& g, const void* q, const void* k, char* ws, const Workspace& L,
+                       double* bound, cudaStream_t st) {
+  unsigned* kmax2 = reinterpret_cast<unsigned*>(ws + L.kmax2);
+  cudaMemsetAsync(kmax2, 0, sizeof(unsigned) * g.Hkv, st);
+  const int per_kv = std::max(1, std::min(ceil_div(g.S, 8), 2 * 148 / std::max(1, g.Hkv) + 1));
+  k_key_norm<<<dim3(per_kv, g.Hkv), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(k), g.S, kmax2);
+  if (int e = check_launch("stage1 key norms")) return e;
+  k_pair_bound<<<g.Hq * g.cn, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(q), g, kmax2, bound);
+  return check_launch("stage1 logit bound");
+}
 
 int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const int* only, char* ws,
                      const Workspace& L, double* col, double* slash, cudaStream_t st) {

@@ -29,7 +29,8 @@ __device__ __forceinline__ bool before(unsigned long long ka, int ia, unsigned l
 
 __global__ void __launch_bounds__(kSelThreads)
     k2_select(const double* __restrict__ col, const double* __restrict__ slash, int cn, int nb,
-              int npow2, double alpha_c, double alpha_s, double eps, int* __restrict__ flags,
+              int npow2, double alpha_c, double alpha_s, double eps, const double* __restrict__ bound,
+              double bound_ref, int* __restrict__ flags,
               const int* __restrict__ only, const int* __restrict__ k_in, int* __restrict__ k_out,
               int* __restrict__ idx_out) {
   extern __shared__ unsigned char smem_raw[];
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(kSelThreads)
     s_k = k;
     k_out[hc * 2 + dir] = k;
     if (eps > 0.0 && k > 0 && flags && !k_in) {
-      const double E = eps * total;
+      // margin widened for large-logit pairs (bound: see k_pair_bound, sa_stage1_tc.cu)
+      const double E = eps * total * (bound ? fmax(1.0, bound[hc] / bound_ref) : 1.0);
       bool close = (cum[k - 1] - target) < E;
       if (k >= 2 && (target - cum[k - 2]) < E) close = true;
       if (k < nb) {
@@ -300,15 +302,15 @@ __global__ void k_check_finite(const uint32_t* __restrict__ x, long long nwords,
 }  // namespace
 
 int launch_select(const double* col, const double* slash, int Hq, int cn, int nb, double ac,
-                  double as, double eps, int* flags, const int* only, const int* k_in, int* k_out,
-                  int* idx_out, cudaStream_t st) {
+                  double as, double eps, const double* bound, double bound_ref, int* flags, const int* only,
+                  const int* k_in, int* k_out, int* idx_out, cudaStream_t st) {
   int npow2 = 1;
   while (npow2 < nb) npow2 <<= 1;
   const size_t smem = (size_t)npow2 * (8 + 8 + 4 + 1);
   if (smem > 220 * 1024) return fail(SA_ERR_UNSUPPORTED, "sa_select: too many blocks (nb > 8192)");
   cudaFuncSetAttribute(k2_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int threads = npow2 >= 2048 ? 1024 : (npow2 >= 64 ? npow2 / 2 : 32);
-  k2_select<<<dim3(2, Hq * cn), threads, smem, st>>>(col, slash, cn, nb, npow2, ac, as, eps, flags,
+  k2_select<<<dim3(2, Hq * cn), threads, smem, st>>>(col, slash, cn, nb, npow2, ac, as, eps, bound, bound_ref, flags,
                                                      only, k_in, k_out, idx_out);
   return check_launch("sa_select");
 }

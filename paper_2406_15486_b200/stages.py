@@ -41,6 +41,11 @@ __all__ = [
 # 5x the worst prefix-sum error of the tensor-core scores measured at 96K-128K
 # (tools/guard_diag.py: max |cum_tc - cum_exact| / total = 7.9e-8)
 GUARD_EPS = 4e-7
+# The tensor-core error grows with sum_i |q_i k_i|, bounded per (head, chunk)
+# by max ||q_r|| * max ||k_j|| / sqrt(d) (sa_stage1's logit bound).  GUARD_EPS
+# applies up to the largest bound of the data it was measured on (GUARD_LOGIT_REF);
+# above it the margin grows in proportion.
+GUARD_LOGIT_REF = 16.0
 
 _WS_CACHE: dict = {}
 
@@ -140,6 +145,7 @@ class ReducedScores:
     col: torch.Tensor
     slash: torch.Tensor
     mode: str
+    logit_bound: torch.Tensor | None = None  # [H, cn] fp64 (tensor mode): the guard's error scale
 
     @property
     def chunks(self) -> tuple:
@@ -152,11 +158,12 @@ class ReducedScores:
         return tuple(ChunkScores(col[c], slash[c], float(col[c].sum())) for c in range(col.shape[0]))
 
 
-def _stage1(b: HeadBatch, plan: ChunkPlan, col, slash, mode: int, only=None) -> None:
+def _stage1(b: HeadBatch, plan: ChunkPlan, col, slash, mode: int, only=None, bound=None) -> None:
     ws = _workspace(b, plan.blk, plan.chunk_n)
     dcall(b.q.device, "sa_stage1", b.q.data_ptr(), b.k.data_ptr(), b.dtype_code, b.S, b.Hq, b.Hkv, b.d, plan.blk,
-              b.group, b.q_head0, plan.chunk_n, plan.itv, col.data_ptr(), slash.data_ptr(), mode,
-              None if only is None else only.data_ptr(), ws.data_ptr(), ws.numel(), b.stream)
+          b.group, b.q_head0, plan.chunk_n, plan.itv, col.data_ptr(), slash.data_ptr(),
+          None if bound is None else bound.data_ptr(), mode, None if only is None else only.data_ptr(),
+          ws.data_ptr(), ws.numel(), b.stream)
 
 
 def block_reduce(samples: SampledScores, blk: int, mode: str | None = None) -> ReducedScores:
@@ -174,8 +181,9 @@ def block_reduce(samples: SampledScores, blk: int, mode: str | None = None) -> R
     nb = n_blocks(b.S, blk)
     col = torch.empty((b.Hq, plan.chunk_n, nb), dtype=torch.float64, device=b.q.device)
     slash = torch.empty_like(col)
-    _stage1(b, plan, col, slash, _lib.SA_STAGE1_TENSOR if mode == "tensor" else _lib.SA_STAGE1_EXACT)
-    return ReducedScores(b.S, blk, plan, b, col, slash, mode)
+    bound = torch.empty((b.Hq, plan.chunk_n), dtype=torch.float64, device=b.q.device) if mode == "tensor" else None
+    _stage1(b, plan, col, slash, _lib.SA_STAGE1_TENSOR if mode == "tensor" else _lib.SA_STAGE1_EXACT, bound=bound)
+    return ReducedScores(b.S, blk, plan, b, col, slash, mode, bound)
 
 
 # ---------------------------------------------------------------- stage 2
@@ -190,7 +198,7 @@ def _vector_select(scores, alpha, k=None):
     k_in = None
     if k is not None:
         k_in = torch.tensor([[[k, k]]], dtype=torch.int32, device=dev)
-    dcall(dev, "sa_select", t.data_ptr(), t.data_ptr(), 1, 1, s.size, alpha, alpha, 0.0, None, None,
+    dcall(dev, "sa_select", t.data_ptr(), t.data_ptr(), 1, 1, s.size, alpha, alpha, 0.0, None, 1.0, None, None,
               None if k_in is None else k_in.data_ptr(), k_out.data_ptr(), idx.data_ptr(),
               torch.cuda.current_stream(dev).cuda_stream)
     kk = int(k_out[0, 0, 0].item())
@@ -252,13 +260,15 @@ def select(reduced: ReducedScores, cfg: SparseConfig, guard: str = "auto",
     idx_sel = torch.empty((H, cn, 2, nb), dtype=torch.int32, device=dev)
     use_guard = guard == "auto" and reduced.mode == "tensor"
     flags = torch.zeros(H * cn, dtype=torch.int32, device=dev) if use_guard else None
+    bound = reduced.logit_bound if use_guard else None
     dcall(dev, "sa_select", reduced.col.data_ptr(), reduced.slash.data_ptr(), H, cn, nb, cfg.alpha_c,
-              cfg.alpha_s, guard_eps if use_guard else 0.0, None if flags is None else flags.data_ptr(),
-              None, None, k_sel.data_ptr(), idx_sel.data_ptr(), st)
+          cfg.alpha_s, guard_eps if use_guard else 0.0, None if bound is None else bound.data_ptr(),
+          GUARD_LOGIT_REF, None if flags is None else flags.data_ptr(), None, None, k_sel.data_ptr(),
+          idx_sel.data_ptr(), st)
     if use_guard:
         _stage1(b, plan, reduced.col, reduced.slash, _lib.SA_STAGE1_EXACT, only=flags)
         dcall(dev, "sa_select", reduced.col.data_ptr(), reduced.slash.data_ptr(), H, cn, nb, cfg.alpha_c,
-                  cfg.alpha_s, 0.0, None, flags.data_ptr(), None, k_sel.data_ptr(), idx_sel.data_ptr(), st)
+              cfg.alpha_s, 0.0, None, 1.0, None, flags.data_ptr(), None, k_sel.data_ptr(), idx_sel.data_ptr(), st)
     return Selection(k_sel, idx_sel, flags, guard)
 
 

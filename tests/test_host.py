@@ -89,23 +89,25 @@ def test_c_abi_rejects_bad_arguments_without_touching_the_gpu():
     lib = _lib.load()
     fake = 0x1000  # never dereferenced: every call below fails validation first
     # stage 1: unsupported tensor-core shape (d != 128), bad plan layout, too small workspace
-    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 2, 1, 64, 128, 2, 0, 1, 4096, fake, fake,
+    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 2, 1, 64, 128, 2, 0, 1, 4096, fake, fake, None,
                        _lib.SA_STAGE1_TENSOR, None, fake, 1 << 30, None)
     assert rc == _lib.SA_ERR_UNSUPPORTED and "d == 128" in _err(lib)
-    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 2, 1, 128, 128, 2, 0, 3, 4000, fake, fake,
+    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 2, 1, 128, 128, 2, 0, 3, 4000, fake, fake, None,
                        _lib.SA_STAGE1_TENSOR, None, fake, 1 << 30, None)
     assert rc == _lib.SA_ERR_INVALID and "plan_chunks" in _err(lib)
-    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 2, 1, 128, 128, 2, 0, 1, 4096, fake, fake,
+    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 2, 1, 128, 128, 2, 0, 1, 4096, fake, fake, None,
                        _lib.SA_STAGE1_TENSOR, None, fake, 16, None)
     assert rc == _lib.SA_ERR_INVALID and "workspace" in _err(lib)
     # GQA mapping past the supplied kv heads
-    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 4, 1, 128, 128, 2, 0, 1, 4096, fake, fake,
+    rc = lib.sa_stage1(fake, fake, _lib.SA_BF16, 4096, 4, 1, 128, 128, 2, 0, 1, 4096, fake, fake, None,
                        _lib.SA_STAGE1_TENSOR, None, fake, 1 << 30, None)
     assert rc == _lib.SA_ERR_INVALID and "kv heads" in _err(lib)
     # stage 2: alpha outside [0, 1] (ref sampler.py:52-56), guard without flags
-    assert lib.sa_select(fake, fake, 1, 1, 8, 1.5, 0.9, 0.0, None, None, None, fake, fake, None) == _lib.SA_ERR_INVALID
+    assert lib.sa_select(fake, fake, 1, 1, 8, 1.5, 0.9, 0.0, None, 1.0, None, None, None, fake, fake, None) == _lib.SA_ERR_INVALID
     assert "alpha_c" in _err(lib)
-    assert lib.sa_select(fake, fake, 1, 1, 8, 0.9, 0.9, 1e-7, None, None, None, fake, fake, None) == _lib.SA_ERR_INVALID
+    assert lib.sa_select(fake, fake, 1, 1, 8, 0.9, 0.9, 1e-7, None, 1.0, None, None, None, fake, fake, None) == _lib.SA_ERR_INVALID
+    assert lib.sa_select(fake, fake, 1, 1, 8, 0.9, 0.9, 1e-7, fake, 0.0, fake, None, None, fake, fake, None) \
+        == _lib.SA_ERR_INVALID and "bound_ref" in _err(lib)
     assert lib.sa_merge(fake, fake, 1, 1, 7, 1024, 128, 1024, 0, 1, fake, fake, None, None, None) == _lib.SA_ERR_INVALID
     assert lib.sa_schedule_len(0, 8, 1, 0) < 0
     assert lib.sa_schedule_len(32, 1024, 16, 0) == 2 * 32 * 1024 // 2

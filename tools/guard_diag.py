@@ -54,3 +54,19 @@ for h in range(Hq):
             m = a_x > 1e-6 * a_x.sum()
             rel.append((np.abs(a_t - a_x)[m] / a_x[m]).max())
 print("per-block relative error quantiles:", np.quantile(rel, [0.5, 0.9, 1.0]))
+
+# error against the per-pair logit bound (sa_stage1's guard scale)
+bnd = rt.logit_bound.cpu().numpy()
+errs = []
+for h in range(Hq):
+    for c in range(plan.chunk_n):
+        e = 0.0
+        for a_t, a_x in ((ct[h, c], cx[h, c]), (st_[h, c], sx[h, c])):
+            tot = a_x.sum()
+            e = max(e, np.abs(np.cumsum(-np.sort(-a_t)) - np.cumsum(-np.sort(-a_x))).max() / tot)
+        errs.append((bnd[h, c], e))
+errs = np.array(errs)
+print("logit bound quantiles:", np.quantile(errs[:, 0], [0.0, 0.5, 1.0]))
+print("prefix-sum error / bound quantiles:", np.quantile(errs[:, 1] / errs[:, 0], [0.5, 0.9, 1.0]))
+print(json.dumps({"S": S, "cn": cn, "bound_max": float(errs[:, 0].max()), "err_max": float(errs[:, 1].max()),
+                  "err_over_bound_max": float((errs[:, 1] / errs[:, 0]).max())}))
