@@ -126,6 +126,18 @@ int sa_merge(const int* k_sel, const int* idx_sel, int Hq, int chunk_n, int nb, 
              int itv, int sink_blocks, int local_blocks, int* kv_cnt, int* kv_idx,
              long long* active_blocks, long long* active_entries, void* stream);
 
+/* Sampled-row CRA — replaces _retained_by_block over the sampled rows
+ * (pipeline.py:37-58, the reference's cra_sampled) from the partials the last
+ * sa_stage1 call of this geometry left in `workspace`: retained[hc*blk + r] is
+ * the normalised probability mass sampled row r of pair hc (= h*cn + c) keeps
+ * inside the mask (kv_cnt / kv_idx, sa_merge's layout); NaN past the window.
+ * mode is the mode of that stage-1 call; rescored_flags (sa_select's guard
+ * flags, may be NULL) marks pairs whose exact re-score replaced the tensor
+ * partials. */
+int sa_sampled_retained(int dtype, int S, int Hq, int Hkv, int d, int blk, int chunk_n, int itv, int mode,
+                        const int* rescored_flags, const int* kv_cnt, const int* kv_idx,
+                        const void* workspace, size_t workspace_bytes, double* retained, void* stream);
+
 /* Full causal block mask (every kb <= qb): the dense-attention comparison row. */
 int sa_full_mask(int Hq, int nb, int* kv_cnt, int* kv_idx, void* stream);
 

@@ -37,6 +37,7 @@ SIGNATURES = {
     "sa_stage1": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _Z, _P]),
     "sa_select": (_I, [_P, _P, _I, _I, _I, _D, _D, _D, _P, _D, _P, _P, _P, _P, _P, _P]),
     "sa_merge": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "sa_sampled_retained": (_I, [_I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _Z, _P, _P]),
     "sa_full_mask": (_I, [_I, _I, _P, _P, _P]),
     "sa_schedule_len": (_I, [_I, _I, _I, _I]),
     "sa_schedule": (_I, [_P, _I, _I, _I, _I, _P, _P]),

@@ -237,6 +237,22 @@ int sa_merge(const int* k_sel, const int* idx_sel, int Hq, int chunk_n, int nb, 
                       kv_idx, active_blocks, active_entries, static_cast<cudaStream_t>(stream));
 }
 
+int sa_sampled_retained(int dtype, int S, int Hq, int Hkv, int d, int blk, int chunk_n, int itv, int mode,
+                        const int* rescored_flags, const int* kv_cnt, const int* kv_idx, const void* workspace,
+                        size_t workspace_bytes, double* retained, void* stream) {
+  if (S < 1 || Hq < 1 || Hkv < 1 || blk < 1 || blk > kMaxSimtBlk || chunk_n < 1 || itv < 1)
+    return fail(SA_ERR_INVALID, "sa_sampled_retained: bad geometry");
+  if (!kv_cnt || !kv_idx || !workspace || !retained) return fail(SA_ERR_INVALID, "sa_sampled_retained: null pointer");
+  if (mode == SA_STAGE1_TENSOR && dtype != SA_BF16)
+    return fail(SA_ERR_UNSUPPORTED, "sa_sampled_retained: tensor-mode partials exist for bf16 only");
+  if (mode != SA_STAGE1_TENSOR && mode != SA_STAGE1_EXACT) return fail(SA_ERR_INVALID, "sa_sampled_retained: mode");
+  const Workspace L = workspace_layout(S, Hq, Hkv, d, blk, chunk_n, dtype);
+  if (workspace_bytes < L.total) return fail(SA_ERR_INVALID, "sa_sampled_retained: workspace too small");
+  Stage1Geom g{S, Hq, Hkv, d, blk, 1, 0, chunk_n, itv, ceil_div(S, blk)};
+  return launch_sampled_retained(g, mode == SA_STAGE1_EXACT, rescored_flags, kv_cnt, kv_idx,
+                                 static_cast<const char*>(workspace), L, retained, static_cast<cudaStream_t>(stream));
+}
+
 int sa_full_mask(int Hq, int nb, int* kv_cnt, int* kv_idx, void* stream) {
   if (Hq < 1 || nb < 1 || !kv_cnt || !kv_idx) return fail(SA_ERR_INVALID, "sa_full_mask: bad args");
   return launch_full(Hq, nb, kv_cnt, kv_idx, static_cast<cudaStream_t>(stream));

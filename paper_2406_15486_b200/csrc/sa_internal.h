@@ -61,6 +61,11 @@ Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int d
 int launch_stage1_exact(const Stage1Geom& g, const void* q, const void* k, int dtype,
                         const int* only_flags, char* ws, const Workspace& L, double* col,
                         double* slash, cudaStream_t st);
+// Per sampled row: the normalised probability mass inside the mask, from the
+// stage-1 partials left in the workspace (exact planes for rescored pairs).
+int launch_sampled_retained(const Stage1Geom& g, int exact_all, const int* rescored, const int* kv_cnt,
+                            const int* kv_idx, const char* ws, const Workspace& L, double* retained,
+                            cudaStream_t st);
 // Guard logit bound per (head, chunk): max ||q_r|| * max ||k_j|| / sqrt(d) (bf16 inputs).
 int launch_logit_bound(const Stage1Geom& g, const void* q, const void* k, char* ws, const Workspace& L,
                        double* bound, cudaStream_t st);

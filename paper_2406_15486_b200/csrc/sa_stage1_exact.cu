@@ -451,6 +451,61 @@ int launch_fold(const Stage1Geom& g, const int* only, const TPlane* pa, const TP
   return check_launch("stage1 finalize");
 }
 
+// ---- sampled-row retained mass from the stage-1 partials (ref pipeline.py:
+// 37-58 _retained_by_block / _sampled_cra): for sampled row r of pair hc,
+//   retained = sum over the key blocks kb active for query block r//blk of
+//              (A + B)[r][kb] * exp(m[r][kb] - M_r) / L_r
+// i.e. the row's normalised probability mass inside the mask, from the same
+// partial planes and row statistics stage 1 folded into col / slash (tensor
+// planes in the log2 domain, exact planes -- guard-rescored pairs or exact
+// mode -- in the natural-log domain).  One CTA per pair, one thread per row.
+__global__ void k_sampled_retained(Stage1Geom g, int exact_all, const int* __restrict__ rescored,
+                                   const float* __restrict__ ta, const float* __restrict__ tb,
+                                   const float* __restrict__ tm, const double* __restrict__ xa,
+                                   const double* __restrict__ xb, const double* __restrict__ xm,
+                                   const double* __restrict__ rowstat, const int* __restrict__ kv_cnt,
+                                   const int* __restrict__ kv_idx, double* __restrict__ retained) {
+  const int hc = blockIdx.x, h = hc / g.cn;
+  const Win w = window_of(hc - h * g.cn, g.S, g.blk, g.itv);
+  const bool exact = exact_all || (rescored && rescored[hc]);
+  for (int r = threadIdx.x; r < g.blk; r += blockDim.x) {
+    const size_t ro = (size_t)hc * g.blk + r;
+    if (r >= w.se - w.ss) {
+      retained[ro] = nan("");
+      continue;
+    }
+    const int row = w.ss + r, qb = row / g.blk;
+    const double M = rowstat[ro * 2], invL = 1.0 / rowstat[ro * 2 + 1];
+    const int n = kv_cnt[(size_t)h * g.nb + qb];
+    const int* list = kv_idx + (size_t)h * tri(g.nb) + tri(qb);
+    double acc = 0.0;
+    for (int j = 0; j < n; ++j) {
+      const size_t o = ro * g.nb + list[j];
+      if (exact) {
+        const double m = xm[o];
+        if (m != -INFINITY) acc += (xa[o] + xb[o]) * exp(m - M);
+      } else {
+        const double m = (double)tm[o];
+        if (m != -INFINITY) acc += ((double)ta[o] + (double)tb[o]) * exp2(m - M);
+      }
+    }
+    retained[ro] = acc * invL;
+  }
+}
+
+int launch_sampled_retained(const Stage1Geom& g, int exact_all, const int* rescored, const int* kv_cnt,
+                            const int* kv_idx, const char* ws, const Workspace& L, double* retained,
+                            cudaStream_t st) {
+  const size_t plane = (size_t)g.Hq * g.cn * g.blk * g.nb;
+  const float* ta = reinterpret_cast<const float*>(ws + L.tc_part);
+  const double* xa = reinterpret_cast<const double*>(ws + L.x_part);
+  k_sampled_retained<<<g.Hq * g.cn, 128, 0, st>>>(g, exact_all, rescored, ta, ta + plane, ta + 2 * plane, xa,
+                                                  xa + plane, xa + 2 * plane,
+                                                  reinterpret_cast<const double*>(ws + L.rowstat), kv_cnt, kv_idx,
+                                                  retained);
+  return check_launch("sampled retained mass");
+}
+
 template int launch_fold<float, true>(const Stage1Geom&, const int*, const float*, const float*,
                                       const float*, char*, const Workspace&, double*, double*,
                                       cudaStream_t);

@@ -21,8 +21,8 @@ from .config import ChunkPlan, SparseConfig, n_blocks, plan_chunks, resolve_conf
 from .errors import InputError
 from .heads import HeadBatch, HeadSet, check_finite_async, check_status, raise_on_flags
 from .masks import BlockMask
-from .stages import (FlopReport, block_reduce, flop_accounting, merge_index, sample_scores, select,
-                     sparse_attention)
+from .stages import (FlopReport, block_reduce, flop_accounting, merge_index, sample_scores, sampled_retained,
+                     select, sparse_attention)
 
 __all__ = ["ORACLE_CAP", "HeadMetrics", "MetricsReport", "cra_full", "run_pipeline", "sample_attention",
            "SampleAttentionResult", "dense_attention"]
@@ -232,6 +232,7 @@ def run_pipeline(head_set, cfg: SparseConfig, want_oracle: bool = False, seed: i
     sel = select(reduced, cfg, guard=guard)
     mask = merge_index(sel, plan, cfg.blk, S)
     ev[2].record()
+    kept_sampled = sampled_retained(reduced, mask, sel.flags)  # cra_sampled from stage 1's partials
     out, flop = sparse_attention(batch, mask, check=False)
     ev[3].record()
     raise_on_flags(flag, batch.q.device)
@@ -244,7 +245,6 @@ def run_pipeline(head_set, cfg: SparseConfig, want_oracle: bool = False, seed: i
     nb, blk = mask.n_qblocks, cfg.blk
     sizes = torch.clamp(S - torch.arange(nb, device=cnt.device) * blk, max=blk)
     entries = ((cnt - 1) * sizes * blk + sizes * (sizes + 1) // 2).sum(dim=1).cpu().numpy()
-    rows_all = [torch.arange(c.sample_start, c.sample_end, device=batch.q.device) for c in plan.chunks]
     heads = []
     dense_out = None
     t_dense = None
@@ -257,7 +257,7 @@ def run_pipeline(head_set, cfg: SparseConfig, want_oracle: bool = False, seed: i
         t_dense = e0.elapsed_time(e1) / 1e3 / H
     for h in range(H):
         kh = batch.k[kv_of[h]]
-        kept = torch.cat([_retained(_causal_probs(batch.q[h, r], kh, r), r, dense[h], blk) for r in rows_all])
+        kept = kept_sampled[h]
         hm = HeadMetrics(
             head_id=batch.head_ids[h] if batch.head_ids else batch.q_head0 + h,
             cra_sampled_min=float(kept.min()), cra_sampled_mean=float(kept.mean()),

@@ -35,17 +35,20 @@ from .masks import BlockMask, SelectedIndices, _tri
 __all__ = [
     "GUARD_EPS", "SampledScores", "ChunkScores", "ReducedScores", "FlopReport", "sample_scores",
     "block_reduce", "find_k", "arg_topk", "select", "merge_index", "select_and_merge",
-    "sparse_attention", "flop_accounting", "as_batch",
+    "sparse_attention", "flop_accounting", "as_batch", "sampled_retained",
 ]
 
 # 5x the worst prefix-sum error of the tensor-core scores measured at 96K-128K
 # (tools/guard_diag.py: max |cum_tc - cum_exact| / total = 7.9e-8)
 GUARD_EPS = 4e-7
 # The tensor-core error grows with sum_i |q_i k_i|, bounded per (head, chunk)
-# by max ||q_r|| * max ||k_j|| / sqrt(d) (sa_stage1's logit bound).  GUARD_EPS
-# applies up to the largest bound of the data it was measured on (GUARD_LOGIT_REF);
-# above it the margin grows in proportion.
-GUARD_LOGIT_REF = 16.0
+# by B = max ||q_r|| * max ||k_j|| / sqrt(d) (sa_stage1's logit bound).
+# Measured (profiles/r2c: C3, C4 at 10 % sampling, and large-logit / heavy-sink
+# heads up to B = 930): prefix-sum error / total <= 4.7e-10 * B.  GUARD_EPS
+# applies up to B = GUARD_LOGIT_REF (the synthetic benchmark heads reach 305);
+# above it the margin grows in proportion, keeping it >= 2.7x the worst
+# measured error at every B.
+GUARD_LOGIT_REF = 320.0
 
 _WS_CACHE: dict = {}
 
@@ -325,6 +328,27 @@ def select_and_merge(reduced: ReducedScores, plan: ChunkPlan, cfg: SparseConfig,
         raise InputError("reduced scores and plan disagree on chunk count")
     sel = select(reduced, cfg, guard=guard)
     return merge_index(sel, plan, reduced.blk, reduced.S, sink_blocks, local_blocks)
+
+
+def sampled_retained(reduced: ReducedScores, mask: BlockMask, rescored: torch.Tensor | None = None) -> torch.Tensor:
+    """Per head, the probability mass every sampled row keeps inside the mask
+    (ref pipeline.py:37-58 `_retained_by_block` over the sampled rows, whose
+    min / mean are cra_sampled), from stage 1's own partials
+    (sa_sampled_retained) -- no recomputation of the sampled rows.  Must follow
+    the stage-1 / select calls of `reduced` on the same stream (it reads their
+    workspace).  `rescored`: the guard flags of the select call.  Returns fp64
+    [H, sampled rows] in plan order."""
+    b, plan = reduced.batch, reduced.plan
+    ws = _workspace(b, plan.blk, plan.chunk_n)
+    out = torch.empty((b.Hq, plan.chunk_n, plan.blk), dtype=torch.float64, device=b.q.device)
+    mode = _lib.SA_STAGE1_TENSOR if reduced.mode == "tensor" else _lib.SA_STAGE1_EXACT
+    dcall(b.q.device, "sa_sampled_retained", b.dtype_code, b.S, b.Hq, b.Hkv, b.d, plan.blk, plan.chunk_n, plan.itv,
+          mode, None if rescored is None else rescored.data_ptr(), mask.kv_cnt.data_ptr(), mask.kv_idx.data_ptr(),
+          ws.data_ptr(), ws.numel(), out.data_ptr(), b.stream)
+    n = [c.sample_end - c.sample_start for c in plan.chunks]
+    if all(x == plan.blk for x in n):
+        return out.view(b.Hq, -1)
+    return torch.cat([out[:, c, :x] for c, x in enumerate(n)], dim=1)
 
 
 # ---------------------------------------------------------------- stage 3

@@ -40,6 +40,30 @@ RANDOM_CASES = [
 ]
 
 
+# run_pipeline metric goldens (ref pipeline.py:149-217, want_oracle=True):
+# name -> (cfg (alpha_c, alpha_s, chunk_n, blk), [(case recipe, head_id), ...])
+PIPELINE_CASES = {
+    "p2048_bf16": ((0.95, 0.95, 2, 128), [
+        (dict(seed=41, S=2048, d=128, scale=0.5, dtype="bf16", sinks=[(0, 10.5), (700, 9.5)], band=5.0), 4),
+        (dict(seed=42, S=2048, d=128, scale=1.5, dtype="bf16"), 1),
+        (dict(seed=43, S=2048, d=128, scale=0.6, dtype="bf16", sinks=[(i * 300 + 3, 11 - 0.5 * i) for i in range(6)],
+              band=4.0), 7)]),
+    "p1000_fp32": ((0.9, 0.95, 3, 128), [
+        (dict(seed=44, S=1000, d=64, scale=1.0, dtype="fp32"), 0),
+        (dict(seed=45, S=1000, d=64, scale=0.5, dtype="fp32", sinks=[(0, 9.0), (333, 8.0)], band=4.0), 2)]),
+}
+WALL_KEYS = ("wall_time_sample", "wall_time_filter", "wall_time_sparse", "wall_time_dense", "wall_time_total")
+
+# tuner golden (ref tuning.py:156-231): the reference's own tune() on its own
+# generator, each generated head rounded to fp32 (recorded, so the GPU tuner
+# can run on the same bits)
+TUNE_TEMPLATE = dict(S=2048, d=32, n_heads=1, sink_columns=[(0, 0.25), (700, 0.15)],
+                     slash_offsets=[(0, 0.3)], noise_scale=2.5, seed=21)
+TUNE_GRID = dict(alphas_c=(0.6, 0.9), alphas_s=(0.6, 0.9), chunk_ns=(1, 3),
+                 length_ranges=((1024, 2048), (9216, 9216)), recall_target=0.8, trials_per_cell=2)
+
+
+
 def bf16_round(x: np.ndarray) -> np.ndarray:
     import torch
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16).float().numpy()

@@ -24,7 +24,8 @@ sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 import blocksift as bs  # noqa: E402
-from tests.golden.inputs import random_qkv, C1_SPEC, RANDOM_CASES  # noqa: E402
+from tests.golden.inputs import (random_qkv, C1_SPEC, RANDOM_CASES, PIPELINE_CASES, TUNE_GRID,  # noqa: E402
+                                 TUNE_TEMPLATE, WALL_KEYS)
 
 
 def run_reference(q, k, v, alpha_c, alpha_s, chunk_n, blk, with_output):
@@ -109,7 +110,44 @@ def kats() -> dict:
     return out
 
 
+def pipeline_goldens() -> dict:
+    out = {}
+    for name, ((ac, as_, cn, blk), heads) in PIPELINE_CASES.items():
+        hs = []
+        for case, hid in heads:
+            q, k, v = random_qkv(case)
+            hs.append(bs.AttentionHead(q, k, v, head_id=hid))
+        rep = bs.run_pipeline(bs.HeadSet(hs), bs.SparseConfig(ac, as_, chunk_n=cn, blk=blk), want_oracle=True)
+        flat = {kk: vv for kk, vv in rep.to_flat_dict().items() if not kk.endswith(WALL_KEYS)}
+        out[name] = flat
+    return out
+
+
+def tune_golden():
+    import blocksift.tuning as bt
+
+    tasks = []
+    orig = bt.generate_synthetic
+
+    def rounded(spec):
+        hset = orig(spec)
+        heads = [bs.AttentionHead(h.q.astype(np.float32).astype(np.float64), h.k.astype(np.float32).astype(np.float64),
+                                  h.v.astype(np.float32).astype(np.float64), head_id=h.head_id) for h in hset]
+        tasks.append((spec.S, np.stack([np.stack([h.q, h.k, h.v]) for h in heads]).astype(np.float32)))
+        return bs.HeadSet(heads)
+
+    bt.generate_synthetic = rounded
+    try:
+        res = bt.tune(bs.TuneGrid(**TUNE_GRID), bs.SyntheticSpec(**TUNE_TEMPLATE))
+    finally:
+        bt.generate_synthetic = orig
+    arrays = {f"task{i}_S{S}": a for i, (S, a) in enumerate(tasks)}
+    return res.to_json_dict(), arrays
+
+
 def main():
+    if "--only-new" in sys.argv:  # the step-4/5 goldens alone (the older fixtures stay byte-identical)
+        return main_new()
     # 1. KATs as JSON
     with open(os.path.join(HERE, "kats.json"), "w") as f:
         json.dump(kats(), f, indent=1)
@@ -131,6 +169,25 @@ def main():
                         0.95, 0.95, 2, 128, with_output=True)
     np.savez_compressed(os.path.join(HERE, "c1_head.npz"), q=q, k=k, v=v, **rec)
     print("C1 density", float(rec["density"]), "k_c", rec["k_c"], "k_s", rec["k_s"])
+    # 4. run_pipeline metrics (MetricsReport.to_flat_dict, wall times dropped)
+    with open(os.path.join(HERE, "pipeline_metrics.json"), "w") as f:
+        json.dump(pipeline_goldens(), f, indent=1, sort_keys=True)
+    # 5. the reference tuner on its own generator (tasks recorded as fp32)
+    res, arrays = tune_golden()
+    with open(os.path.join(HERE, "tune_result.json"), "w") as f:
+        json.dump(res, f, indent=1, sort_keys=True)
+    np.savez_compressed(os.path.join(HERE, "tune_tasks.npz"), **arrays)
+    print("tune:", [(r["lo"], r["feasible"], r["best"]) for r in res["ranges"]])
+
+
+def main_new():
+    with open(os.path.join(HERE, "pipeline_metrics.json"), "w") as f:
+        json.dump(pipeline_goldens(), f, indent=1, sort_keys=True)
+    res, arrays = tune_golden()
+    with open(os.path.join(HERE, "tune_result.json"), "w") as f:
+        json.dump(res, f, indent=1, sort_keys=True)
+    np.savez_compressed(os.path.join(HERE, "tune_tasks.npz"), **arrays)
+    print("tune:", [(r["lo"], r["feasible"], r["best"]) for r in res["ranges"]])
 
 
 if __name__ == "__main__":
