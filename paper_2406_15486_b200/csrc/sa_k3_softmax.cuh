@@ -68,14 +68,23 @@ struct K3Prof {
 #endif
 };
 
-// Fraction of off-diagonal exponentials computed by the FMA-pipe polynomial
-// (SA_K3_POLY n -> n/4 of the pairs; product 0).
-#ifndef SA_K3_POLY
-#define SA_K3_POLY 0
+// Exponentials moved from the MUFU pipe to the FMA pipe (ex2_poly2_floor):
+// per 128-key block the two softmax warps of an SM sub-partition need 8192
+// MUFU ex2 (2048 cycles at 4/clk), exactly the 2048 cycles of tensor work of
+// the step, so a share of emulated pairs gives the MUFU slack.  A pair (t in
+// 0..15) of 32-key fragment fr (0..3) is emulated when bit fr of
+// SA_K3_EMU_FRAG and bit t of SA_K3_EMU_T are set.  Product: fragments 1 and 2,
+// pairs 6, 7, 14, 15 = 1/8 of the exponentials (A/B in DESIGN.md §3.1).
+#ifndef SA_K3_EMU_FRAG
+#define SA_K3_EMU_FRAG 0x6
+#endif
+#ifndef SA_K3_EMU_T
+#define SA_K3_EMU_T 0xC0C0
 #endif
 
-__device__ __forceinline__ uint64_t k3_exp_pair(float y0, float y1, int t) {
-  return ((t & 3) >= 4 - SA_K3_POLY) ? ex2_poly2(y0, y1) : f32x2(ex2(y0), ex2(y1));
+__device__ __forceinline__ uint64_t k3_exp_pair(float y0, float y1, int fr, int t) {
+  return (((SA_K3_EMU_FRAG >> fr) & 1) && ((SA_K3_EMU_T >> t) & 1)) ? ex2_poly2_floor(y0, y1)
+                                                                     : f32x2(ex2(y0), ex2(y1));
 }
 
 __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBars& b, uint32_t tS0,
@@ -128,7 +137,7 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
         tmem_ld32(tS + h * 64, buf[0]);
         tmem_ld32(tS + h * 64 + 32, buf[1]);
       };
-      auto half_exps = [&](float m, float& ymax) {
+      auto half_exps = [&](int h, float m, float& ymax) {
         const uint64_t negm = f32x2(-m, -m);
         bacc0 = f32x2(0.f, 0.f);
         bacc1 = f32x2(0.f, 0.f);
@@ -144,7 +153,7 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
                                negm),
                          y0, y1);
             ymax = fmax3(ymax, y0, y1);
-            const uint64_t pp = k3_exp_pair(y0, y1, t);
+            const uint64_t pp = k3_exp_pair(y0, y1, 2 * h + ch, t);
             if (t & 1)
               bacc1 = fadd2(bacc1, pp);
             else
@@ -166,14 +175,14 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
       };
       float ymax;
       load_half(0);
-      half_exps(m_ref, ymax);
+      half_exps(0, m_ref, ymax);
       if (!__any_sync(0xffffffffu, ymax > kK3RescaleThreshold)) {
         store_half(0);
         arrive(b.p_part);
         lacc0 = fadd2(lacc0, bacc0);
         lacc1 = fadd2(lacc1, bacc1);
         load_half(1);
-        half_exps(m_ref, ymax);
+        half_exps(1, m_ref, ymax);
         if (__any_sync(0xffffffffu, ymax > kK3RescaleThreshold)) {
           k3_wait(b.pv_half, j & 1);  // O now holds every PV up to this block's keys 0..63
           pv_seen = j + 1;
@@ -206,7 +215,7 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
           }
           m_ref = m_new;
           load_half(1);
-          half_exps(m_ref, ymax);  // with the row max of keys 64..127 every exponent is <= 0
+          half_exps(1, m_ref, ymax);  // with the row max of keys 64..127 every exponent is <= 0
         }
         store_half(1);
         arrive(b.p_full);
@@ -308,7 +317,7 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
             float y0, y1;
             unpack_f32x2(ffma2(f32x2(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1])), sl2x2, negm),
                          y0, y1);
-            const uint64_t pp = k3_exp_pair(y0, y1, t);
+            const uint64_t pp = k3_exp_pair(y0, y1, ch, t);
             if (t & 1)
               lacc1 = fadd2(lacc1, pp);
             else

@@ -408,55 +408,37 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
   return d;
 }
 
-// 2^x for a pair on the FMA pipe (offloads the MUFU unit): round-to-nearest
-// split x = j + f via the 1.5*2^23 magic constant, degree-3 minimax
-// polynomial for 2^f on [-0.5, 0.5] (max rel. error 7.5e-5, far below the
-// bf16 rounding of P), exponent added as an integer.  x is clamped at -127
-// (no -inf inputs: callers use it only on unmasked tiles).
-__device__ __forceinline__ uint64_t ex2_poly2(float x0, float x1) {
+// 2^x for a pair on the FMA pipe, floor split: x = j + f with j = floor(x)
+// (add.rm against 1.5*2^23), f in [0, 1), degree-3 fit of 2^f on [0, 1)
+// (max rel. error ~9e-5, below bf16's 2^-9 rounding of P), exponent added with
+// shl + add on the integer ALU (LEA), not IMAD, so the FMA pipe only carries
+// the 2 packed adds and 4 packed FMAs.  x is clamped at -127.
+__device__ __forceinline__ uint64_t ex2_poly2_floor(float x0, float x1) {
   const float kMagic = 12582912.0f;
   x0 = fmaxf(x0, -127.f);
   x1 = fmaxf(x1, -127.f);
   const uint64_t X = f32x2(x0, x1);
-  const uint64_t T = fadd2(X, f32x2(kMagic, kMagic));
+  uint64_t T;
+  asm("add.rm.ftz.f32x2 %0, %1, %2;" : "=l"(T) : "l"(X), "l"(f32x2(kMagic, kMagic)));
   const uint64_t J = fadd2(T, f32x2(-kMagic, -kMagic));
   const uint64_t F = ffma2(J, f32x2(-1.f, -1.f), X);
-  uint64_t P = ffma2(F, f32x2(0.05517132f, 0.05517132f), f32x2(0.24261054f, 0.24261054f));
-  P = ffma2(P, F, f32x2(0.69326099f, 0.69326099f));
-  P = ffma2(P, F, f32x2(0.99992811f, 0.99992811f));
+  uint64_t P = ffma2(F, f32x2(0.07802286f, 0.07802286f), f32x2(0.22606719f, 0.22606719f));
+  P = ffma2(P, F, f32x2(0.69583483f, 0.69583483f));
+  P = ffma2(P, F, f32x2(0.99992493f, 0.99992493f));
   uint32_t p0, p1, t0, t1;
   asm("mov.b64 {%0, %1}, %2;" : "=r"(p0), "=r"(p1) : "l"(P));
   asm("mov.b64 {%0, %1}, %2;" : "=r"(t0), "=r"(t1) : "l"(T));
-  asm("mad.lo.u32 %0, %1, 8388608, %0;" : "+r"(p0) : "r"(t0));
-  asm("mad.lo.u32 %0, %1, 8388608, %0;" : "+r"(p1) : "r"(t1));
+  p0 += t0 << 23;
+  p1 += t1 << 23;
   uint64_t r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(p0), "r"(p1));
   return r;
-}
-
-// 2^x for a pair on ONE MUFU op: f32x2 -> f16x2, ex2.approx.f16x2, back to
-// f32x2 (a probability that is rounded to bf16 for the PV MMA anyway; inputs
-// below -24 flush to 0).
-__device__ __forceinline__ uint64_t ex2_h2(float x0, float x1) {
-  uint32_t h, e;
-  asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(x0), "f"(x1));
-  asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
-  float y0, y1;
-  asm("{\n\t.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
-      : "=f"(y0), "=f"(y1)
-      : "r"(e));
-  return f32x2(y0, y1);
 }
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-}
-// bf16x2 pack on the integer ALU (round half up; valid for finite x >= 0,
-// i.e. softmax probabilities) -- keeps the conversion off the MUFU/XU pipe.
-__device__ __forceinline__ uint32_t pack_bf16_pos(float lo, float hi) {
-  return __byte_perm(__float_as_uint(lo) + 0x8000u, __float_as_uint(hi) + 0x8000u, 0x7632);
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;

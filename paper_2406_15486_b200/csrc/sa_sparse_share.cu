@@ -35,6 +35,7 @@ namespace {
 // warp 0 TMA, warp 1 MMA, warps 2-3 idle (so each softmax warpgroup starts at
 // TMEM lane quadrant 0), then the softmax warps: 4-7 for A and 8-11 for B.
 constexpr int kWarps = 12;
+
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kTileBytes = 128 * 128 * 2;
 constexpr uint32_t kBoxBytes = kTileBytes / 2;
@@ -243,6 +244,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       n_pv[x] = j + 1;
     };
+    // S_X(step) from K slot `slot`: 8 K-steps of 16 into TMEM S_X, then s_full[X]
+    auto issue_s = [&](int x, int slot) {
+      pf.start();
+      if (n_s[x] == 0) k3_wait(&sm->q_full[x], 0);
+      pf.stop(9);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
+          umma_ss(tS[x], q_desc[x] + (off >> 4), k_desc0 + ((slot * kTileBytes + off) >> 4), kIdescQK,
+                  kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&sm->s_full[x]);
+      }
+      __syncwarp();
+      ++n_s[x];
+    };
     while (w.next(kb, in[0], in[1])) {
       const int s = t & 1;
       pf.start();
@@ -255,21 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pend[x] = -1;
         }
         if (in[x]) {
-          pf.start();
-          if (n_s[x] == 0) k3_wait(&sm->q_full[x], 0);
-          pf.stop(9);
-          tc_fence_after();
-          if (elect_one()) {
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint32_t off = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
-              umma_ss(tS[x], q_desc[x] + (off >> 4), k_desc0 + ((s * kTileBytes + off) >> 4),
-                      kIdescQK, kk > 0 ? 1u : 0u);
-            }
-            umma_commit(&sm->s_full[x]);
-          }
-          __syncwarp();
-          ++n_s[x];
+          issue_s(x, s);
           pend[x] = t;
         }
       }
