@@ -47,7 +47,35 @@ CONFIGS = {
     "c2": (32768, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 32K, bf16, alpha 0.95, chunk_n 1"),
     "c4": (98304, 32, 8, 0.95, 15, "InternLM2-7B attention shape, seq 96K, bf16, alpha 0.95, 2% sampling"),
     "c5": (1048576, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 1M, bf16, alpha 0.95, heads sharded + NVLink gather"),
+    # the same shapes on heads from the reference's OWN calibrated generator (refsynth: SURVEY.md's C1 family of
+    # planted structures, one calibrated head per KV group, q heads redraw their noise dims)
+    "c2ref": (32768, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 32K, bf16, alpha 0.95, chunk_n 1, "
+                                     "reference-calibrated heads"),
+    "c3ref": (131072, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 128K, bf16, alpha 0.95, chunk_n 1, "
+                                      "reference-calibrated heads"),
 }
+# planted structures of the *ref configs (SURVEY.md section 8d, C1 family: sinks at 0 and 1500, local window)
+REF_SINKS = ((0, 0.18), (1500, 0.14))
+REF_SLASHES = ((0, 0.60),)
+
+
+def workload_inputs(config, S, Hq, Hkv, d, seed, heads, device):
+    """(q, k, v, kv_heads, data description) for the given global q heads."""
+    import torch
+
+    from paper_2406_15486_b200 import refsynth, synth
+    if not config.endswith("ref"):
+        q, k, v, kv = synth.make_inputs(S, Hq, Hkv, d, seed=seed, heads=heads, device=device)
+        return q, k, v, kv, "synthetic (seeded GPU generator: Zipf column sinks + local band + slash band + noise)"
+    spec = refsynth.SyntheticSpec(S, d, Hkv, REF_SINKS, REF_SLASHES, 1.0, seed)
+    q, k, v, _ = refsynth.calibrated_gqa_inputs(spec, Hq, Hkv, dtype=torch.bfloat16, device=device)
+    group = Hq // Hkv
+    kv = sorted({h // group for h in heads})
+    q = q[heads].contiguous()
+    k, v = k[kv].contiguous(), v[kv].contiguous()
+    return q, k, v, kv, (f"synthetic (the reference's calibrated generator restated on the GPU, "
+                         f"sinks {list(REF_SINKS)}, slash offsets {list(REF_SLASHES)}, one calibrated head per KV "
+                         f"group, q heads redraw their noise dims)")
 
 
 def peaks():
@@ -246,7 +274,7 @@ def main():
     per = Hq // world
     my_heads = list(range(rank * per, (rank + 1) * per))
     group = Hq // Hkv
-    q, k, v, kv_heads = synth.make_inputs(S, Hq, Hkv, d, seed=args.seed, heads=my_heads, device=dev)
+    q, k, v, kv_heads, data_desc = workload_inputs(args.config, S, Hq, Hkv, d, args.seed, my_heads, dev)
     q_head0 = my_heads[0]
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     out = torch.empty_like(q)
@@ -416,7 +444,7 @@ def main():
                 "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(t_max, 3), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-                "data": "synthetic (seeded GPU generator: Zipf column sinks + local band + slash band + noise)",
+                "data": data_desc,
                 "config": workload, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(),
                 "launch_path": "CUDA graphs (SampleAttentionGraph)" if gexec is not None else "eager", **extra}
@@ -565,12 +593,10 @@ def run_reference(args, rank, S, Hq, Hkv, d, alpha, chunk_n, workload):
         return
     import torch
 
-    from paper_2406_15486_b200 import synth
-
     # the same bits our arm times: the seeded generator runs where our arm runs it (input plumbing,
     # untimed); the reference algorithm itself only ever runs on the host
     gen_dev = "cuda" if torch.cuda.is_available() else "cpu"
-    q, k, v, kv = synth.make_inputs(S, Hq, Hkv, d, seed=args.seed, heads=[0], device=gen_dev)
+    q, k, v, kv, _ = workload_inputs(args.config, S, Hq, Hkv, d, args.seed, [0], gen_dev)
     qh, kh, vh = (t[0].double().cpu().numpy() for t in (q, k, v))
     del q, k, v
     runs = []

@@ -148,9 +148,13 @@ int sa_full_mask(int Hq, int nb, int* kv_cnt, int* kv_idx, void* stream);
  * order[2*u], order[2*u+1] = h*nb + qb of unit u's items (-1: no partner),
  * grouped by KV head (one KV head's K/V stays L2-resident while its units run)
  * and longest-first (descending kv_cnt[a] + kv_cnt[b]) inside a group.
+ * With kv_idx and scratch (sa_schedule_len ints) the q heads of a group are
+ * paired per query block by list overlap (fewest key blocks listed by only one
+ * of the two); with either NULL they pair as (h, h+1).
  * sa_schedule_len returns the entry count 2 * n_units (or < 0 on bad args). */
 int sa_schedule_len(int Hq, int nb, int group, int q_head0);
-int sa_schedule(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* order, void* stream);
+int sa_schedule(const int* kv_cnt, const int* kv_idx, int Hq, int nb, int group, int q_head0, int* order,
+                int* scratch, void* stream);
 
 /* Stage 3 — replaces sparse_attention (executor.py:104-158): per (head,
  * query block) the online-softmax recurrence over the mask's ascending key

@@ -40,7 +40,7 @@ SIGNATURES = {
     "sa_sampled_retained": (_I, [_I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _Z, _P, _P]),
     "sa_full_mask": (_I, [_I, _I, _P, _P, _P]),
     "sa_schedule_len": (_I, [_I, _I, _I, _I]),
-    "sa_schedule": (_I, [_P, _I, _I, _I, _I, _P, _P]),
+    "sa_schedule": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P]),
     "sa_sparse_forward": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
 }
 

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <set>
 #include <tuple>
@@ -27,7 +28,8 @@ int launch_merge(const int* k_sel, const int* idx_sel, int Hq, int cn, int nb, i
                  int itv, int sink_blocks, int local_blocks, int* kv_cnt, int* kv_idx,
                  long long* ab, long long* ae, cudaStream_t st);
 int launch_full(int Hq, int nb, int* kv_cnt, int* kv_idx, cudaStream_t st);
-int launch_sched(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* order, cudaStream_t st);
+int launch_sched(const int* kv_cnt, const int* kv_idx, int Hq, int nb, int group, int q_head0, int* order,
+                 int* scratch, cudaStream_t st);
 int launch_check_finite(const void* x, int dtype, long long n, int* flag, cudaStream_t st);
 
 namespace {
@@ -81,14 +83,19 @@ unsigned* status_ptr() {
 }
 
 void set_smem_attr(const void* fn, int bytes) {
+  // The opt-in is a ceiling: keep the largest size set per (kernel, device)
+  // and only ever raise it, so a call with a smaller size cannot lower the
+  // limit under a later, larger launch.
   static std::mutex mu;
-  static std::set<std::tuple<const void*, int, int>> done;
+  static std::map<std::pair<const void*, int>, int> ceiling;
   int dev = 0;
   cudaGetDevice(&dev);
-  const auto key = std::make_tuple(fn, dev, bytes);
+  const auto key = std::make_pair(fn, dev);
   std::lock_guard<std::mutex> lock(mu);
-  if (done.count(key)) return;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess) done.insert(key);
+  auto it = ceiling.find(key);
+  if (it != ceiling.end() && it->second >= bytes) return;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess)
+    ceiling[key] = bytes;
 }
 
 bool make_tmap_bf16_hsd(CUtensorMap* map, const void* base, int H, int S, int d, int box_rows) {
@@ -258,10 +265,11 @@ int sa_full_mask(int Hq, int nb, int* kv_cnt, int* kv_idx, void* stream) {
   return launch_full(Hq, nb, kv_cnt, kv_idx, static_cast<cudaStream_t>(stream));
 }
 
-int sa_schedule(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* order, void* stream) {
+int sa_schedule(const int* kv_cnt, const int* kv_idx, int Hq, int nb, int group, int q_head0, int* order,
+                int* scratch, void* stream) {
   if (Hq < 1 || nb < 1 || !kv_cnt || !order) return fail(SA_ERR_INVALID, "sa_schedule: bad args");
   if (group < 1 || q_head0 < 0) return fail(SA_ERR_INVALID, "sa_schedule: bad group / q_head0");
-  return launch_sched(kv_cnt, Hq, nb, group, q_head0, order, static_cast<cudaStream_t>(stream));
+  return launch_sched(kv_cnt, kv_idx, Hq, nb, group, q_head0, order, scratch, static_cast<cudaStream_t>(stream));
 }
 
 int sa_schedule_len(int Hq, int nb, int group, int q_head0) {

@@ -15,8 +15,9 @@ namespace sa {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int check_launch(const char* what);
-// Opt `fn` into `bytes` of dynamic shared memory on the CURRENT device.  The
-// attribute is per device, so the opt-in is cached per (kernel, device, size).
+// Opt `fn` into at least `bytes` of dynamic shared memory on the CURRENT
+// device.  The attribute is per device and a ceiling, so the largest size set
+// is kept per (kernel, device) and only ever raised.
 void set_smem_attr(const void* fn, int bytes);
 
 // Device status word behind sa_status(): [0] OR of the SA_STATUS_* bits,

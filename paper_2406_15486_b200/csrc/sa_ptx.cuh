@@ -415,8 +415,8 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
 // the 2 packed adds and 4 packed FMAs.  x is clamped at -127.
 __device__ __forceinline__ uint64_t ex2_poly2_floor(float x0, float x1) {
   const float kMagic = 12582912.0f;
-  x0 = fmaxf(x0, -127.f);
-  x1 = fmaxf(x1, -127.f);
+  x0 = fmaxf(x0, -125.f);  // -127 would put 2^-127 * 0.9999 past the exponent field (NaN)
+  x1 = fmaxf(x1, -125.f);
   const uint64_t X = f32x2(x0, x1);
   uint64_t T;
   asm("add.rm.ftz.f32x2 %0, %1, %2;" : "=l"(T) : "l"(X), "l"(f32x2(kMagic, kMagic)));

@@ -228,12 +228,94 @@ __global__ void k2_full(int Hq, int nb, int* __restrict__ kv_cnt, int* __restric
   if (threadIdx.x == 0) kv_cnt[item] = qb + 1;
 }
 
+// Stage-3 unit pairing by list overlap.  A unit's CTA walks the UNION of its two
+// items' key-block lists, and a union step listed by only one item leaves the
+// other item's softmax idle and its chain exposed.  The heads of one KV group
+// at one query block have different lists (stage 2 selects per head), so which
+// heads share a unit matters: one CTA per (query block, local KV group) builds
+// the group's key-block bitmaps, the symmetric difference |A xor B| of every
+// head pair, and matches the heads greedily (smallest difference first, ties
+// by head index).  At C3 this halves the one-item steps (17.6 % -> 8.4 % of the
+// union steps) against the fixed (2p, 2p+1) pairing.  An odd group keeps its
+// last head for the adjacent-query-block units of unit_items.
+constexpr int kPairMaxHeads = 64;
+
+__global__ void __launch_bounds__(256) k2_pair(const int* __restrict__ kv_cnt, const int* __restrict__ kv_idx,
+                                               int Hq, int nb, int group, int q_head0, int* __restrict__ pairs) {
+  extern __shared__ unsigned bm[];  // [m][W] key-block bitmaps, then [m*(m-1)/2] pair differences
+  const int qb = blockIdx.x, g = blockIdx.y;
+  int lo, hi;
+  kv_group_heads(g, Hq, group, q_head0, lo, hi);
+  const int m = (hi - lo) & ~1;
+  if (m < 2) return;
+  int base = 0;
+  for (int x = 0; x < g; ++x) {
+    int l2, h2;
+    kv_group_heads(x, Hq, group, q_head0, l2, h2);
+    base += units_of_group(h2 - l2, nb);
+  }
+  const int W = (qb >> 5) + 1;
+  unsigned* diff = bm + m * W;
+  const int np = m * (m - 1) / 2;
+  for (int i = threadIdx.x; i < m * W; i += blockDim.x) bm[i] = 0u;
+  __syncthreads();
+  for (int i = 0; i < m; ++i) {
+    const int item = (lo + i) * nb + qb;
+    const int n = min(max(__ldg(kv_cnt + item), 0), qb + 1);
+    const int* list = kv_idx + (size_t)(lo + i) * tri(nb) + tri(qb);
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+      const int kb = __ldg(list + e);
+      if (kb >= 0 && kb <= qb) atomicOr(bm + i * W + (kb >> 5), 1u << (kb & 31));
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int t = warp; t < np; t += nwarps) {
+    int i = 0, r = t;  // t -> (i, j), i < j, row-major over the upper triangle
+    while (r >= m - 1 - i) {
+      r -= m - 1 - i;
+      ++i;
+    }
+    const int j = i + 1 + r;
+    int c = 0;
+    for (int w = lane; w < W; w += 32) c += __popc(bm[i * W + w] ^ bm[j * W + w]);
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) diff[t] = (unsigned)c;
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  unsigned long long used = 0ull;
+  for (int p = 0; p < m / 2; ++p) {
+    // key = difference (<= nb < 2^20), then i, then j: the smallest key wins
+    unsigned best = 0xffffffffu;
+    for (int t = lane; t < np; t += 32) {
+      int i = 0, r = t;
+      while (r >= m - 1 - i) {
+        r -= m - 1 - i;
+        ++i;
+      }
+      const int j = i + 1 + r;
+      if (((used >> i) & 1ull) || ((used >> j) & 1ull)) continue;
+      best = min(best, (diff[t] << 12) | (unsigned)(i << 6) | (unsigned)j);
+    }
+    best = __reduce_min_sync(0xffffffffu, best);
+    const int i = (best >> 6) & 63, j = best & 63;
+    used |= (1ull << i) | (1ull << j);
+    if (lane == 0) {
+      const size_t u = (size_t)base + (size_t)p * nb + qb;
+      pairs[2 * u] = (lo + i) * nb + qb;
+      pairs[2 * u + 1] = (lo + j) * nb + qb;
+    }
+  }
+}
+
 // Stage-3 work units (sa_internal.h: two items of one KV head per unit),
 // counting-sorted by descending cost kv_cnt[a] + kv_cnt[b], one CTA per local
 // KV group.  Group-major keeps one KV head's K/V (64 MiB at 128K) resident in
 // L2 while its units run; longest-first inside a group evens out the tail.
+// With `pairs` (k2_pair's matching) the paired units take their items from it.
 __global__ void __launch_bounds__(1024) k2_units(const int* __restrict__ kv_cnt, int Hq, int nb, int group,
-                                                 int q_head0, int* __restrict__ units) {
+                                                 int q_head0, const int* __restrict__ pairs, int* __restrict__ units) {
   extern __shared__ int hist[];  // [2 * nb + 2]
   int h_lo, h_hi;
   kv_group_heads(blockIdx.x, Hq, group, q_head0, h_lo, h_hi);
@@ -246,12 +328,21 @@ __global__ void __launch_bounds__(1024) k2_units(const int* __restrict__ kv_cnt,
     base += units_of_group(hi - lo, nb);
   }
   const int nu = units_of_group(nh, nb);
+  const int paired = (nh / 2) * nb;
   const int nbins = 2 * nb + 2;
   for (int i = threadIdx.x; i < nbins; i += blockDim.x) hist[i] = 0;
   __syncthreads();
+  auto items = [&](int u, int& a, int& b) {
+    if (pairs && u < paired) {
+      a = __ldg(pairs + 2 * (base + u));
+      b = __ldg(pairs + 2 * (base + u) + 1);
+    } else {
+      unit_items(u, h_lo, nh, nb, a, b);
+    }
+  };
   auto cost = [&](int u) {
     int a, b;
-    unit_items(u, h_lo, nh, nb, a, b);
+    items(u, a, b);
     const int c = max(kv_cnt[a], 0) + (b >= 0 ? max(kv_cnt[b], 0) : 0);
     return min(c, nbins - 1);
   };
@@ -269,7 +360,7 @@ __global__ void __launch_bounds__(1024) k2_units(const int* __restrict__ kv_cnt,
   for (int u = threadIdx.x; u < nu; u += blockDim.x) {
     const int slot = atomicAdd(hist + cost(u), 1);
     int a, b;
-    unit_items(u, h_lo, nh, nb, a, b);
+    items(u, a, b);
     units[2 * slot] = a;
     units[2 * slot + 1] = b;
   }
@@ -334,11 +425,29 @@ int launch_full(int Hq, int nb, int* kv_cnt, int* kv_idx, cudaStream_t st) {
   return check_launch("sa_full_mask");
 }
 
-int launch_sched(const int* kv_cnt, int Hq, int nb, int group, int q_head0, int* units, cudaStream_t st) {
+int launch_sched(const int* kv_cnt, const int* kv_idx, int Hq, int nb, int group, int q_head0, int* units,
+                 int* scratch, cudaStream_t st) {
   const size_t smem = (size_t)(2 * nb + 2) * 4;
   if (smem > 200 * 1024) return fail(SA_ERR_UNSUPPORTED, "sa_schedule: nb too large");
-  cudaFuncSetAttribute(k2_units, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k2_units<<<n_local_kv(Hq, group, q_head0), 1024, smem, st>>>(kv_cnt, Hq, nb, group, q_head0, units);
+  const int G = n_local_kv(Hq, group, q_head0);
+  const int* pairs = nullptr;
+  if (kv_idx && scratch) {
+    int m = 0;  // largest matched head count of a local group
+    for (int g = 0; g < G; ++g) {
+      int lo, hi;
+      kv_group_heads(g, Hq, group, q_head0, lo, hi);
+      m = std::max(m, (hi - lo) & ~1);
+    }
+    const size_t psmem = ((size_t)m * ((nb + 31) / 32) + (size_t)m * (m - 1) / 2) * 4;
+    if (m >= 4 && m <= kPairMaxHeads && psmem <= 200 * 1024) {  // m == 2 has one possible pairing
+      set_smem_attr(reinterpret_cast<const void*>(&k2_pair), (int)psmem);
+      k2_pair<<<dim3(nb, G), 256, psmem, st>>>(kv_cnt, kv_idx, Hq, nb, group, q_head0, scratch);
+      if (int e = check_launch("sa_schedule (pairing)")) return e;
+      pairs = scratch;
+    }
+  }
+  set_smem_attr(reinterpret_cast<const void*>(&k2_units), (int)smem);
+  k2_units<<<G, 1024, smem, st>>>(kv_cnt, Hq, nb, group, q_head0, pairs, units);
   return check_launch("sa_schedule");
 }
 

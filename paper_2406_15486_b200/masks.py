@@ -266,8 +266,9 @@ class BlockMask:
 
     # ------------------------------------------------------------ scheduling
     def order(self, group: int = 1, q_head0: int = 0) -> torch.Tensor:
-        """Stage-3 work units (sa_schedule): pairs of items sharing a KV head,
-        KV-group-major and longest-first; cached per (group, q_head0)."""
+        """Stage-3 work units (sa_schedule): pairs of items sharing a KV head
+        (q heads matched per query block by list overlap), KV-group-major and
+        longest-first; cached per (group, q_head0)."""
         key = (group, q_head0)
         if self._order is None or self._order[0] != key:
             nb = self.n_qblocks
@@ -275,7 +276,9 @@ class BlockMask:
             if n < 0:
                 raise InputError(f"bad schedule geometry (heads {self.n_heads}, group {group}, q_head0 {q_head0})")
             order = torch.empty(n, dtype=torch.int32, device=self.device)
-            dcall(self.device, "sa_schedule", self.kv_cnt.data_ptr(), self.n_heads, nb, group, q_head0,
-                  order.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
+            scratch = torch.empty(n, dtype=torch.int32, device=self.device)  # the overlap pairing
+            dcall(self.device, "sa_schedule", self.kv_cnt.data_ptr(), self.kv_idx.data_ptr(), self.n_heads, nb,
+                  group, q_head0, order.data_ptr(), scratch.data_ptr(),
+                  torch.cuda.current_stream(self.device).cuda_stream)
             self._order = (key, order)
         return self._order[1]

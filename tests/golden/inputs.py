@@ -106,3 +106,21 @@ def random_qkv(case: dict):
     else:
         q, k, v = (a.astype(np.float32) for a in (q, k, v))
     return q.astype(np.float64), k.astype(np.float64), v.astype(np.float64)
+
+
+# ---- calibrated generator (ref synth.py): specs for tests/golden/refsynth.json
+REFSYNTH_SPECS = [
+    dict(S=1024, d=64, n_heads=2, sink_columns=((0, 0.2), (300, 0.1)), slash_offsets=((0, 0.5),), seed=3),
+    dict(S=2048, d=128, n_heads=2, sink_columns=((0, 0.18), (1500, 0.14)), slash_offsets=((0, 0.60),), seed=0),
+    dict(S=1536, d=128, n_heads=1, sink_columns=((0, 0.15),), slash_offsets=((0, 0.4), (300, 0.1)), seed=5),
+    dict(S=3000, d=96, n_heads=1, sink_columns=((10, 0.1), (2000, 0.05)), slash_offsets=((0, 0.3), (700, 0.15)),
+         noise_scale=1.5, seed=11),
+]
+REFSYNTH_BAD_SPECS = [
+    dict(S=1024, d=64, sink_columns=((1020, 0.2),)),                   # no measurement rows past the sink
+    dict(S=1024, d=64, sink_columns=((0, 0.6),), slash_offsets=((0, 0.6),)),   # masses sum past 1
+    dict(S=1024, d=64, slash_offsets=((0, 0.3), (10, 0.2))),           # offsets too close to separate
+    dict(S=1024, d=8, sink_columns=((0, 0.2),), slash_offsets=((0, 0.3),)),    # reserved dims exceed d
+    dict(S=1024, d=64, sink_columns=((5, 0.2), (5, 0.1))),             # duplicate sink
+    dict(S=64, d=64, sink_columns=((0, 0.9),), noise_scale=3.0, seed=1),  # calibration target out of reach?
+]

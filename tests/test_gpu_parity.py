@@ -464,3 +464,53 @@ def test_guard_auto_matches_always_at_large_logits(sa, seed, scale, sink):
         assert ra.mask.selections() == rw.mask.selections(), (alpha, ra.n_rescored())
         ref = O.run_head(q, k, None, alpha, alpha, cn, 128, with_output=False)
         assert [(c.i_c, c.i_s) for c in rw.mask.selections()[0].chunks] == ref["selection"], alpha
+
+
+@pytest.mark.parametrize("Hq,Hkv,S", [(32, 2, 16384), (12, 2, 4096), (10, 2, 4096), (16, 4, 8192)])
+def test_schedule_overlap_pairing(sa, Hq, Hkv, S):
+    """sa_schedule's overlap pairing: every (head, query block) item appears in
+    exactly one unit, both items of a unit read the same KV head (same query
+    block for head pairs; adjacent query blocks for an odd group's last head),
+    costs descend inside each KV group, no pairing leaves more one-item union
+    steps than the fixed (2p, 2p+1) pairing, and the stage-3 output is the
+    same whichever order runs it."""
+    from paper_2406_15486_b200 import _lib
+    from paper_2406_15486_b200 import synth
+    q, k, v, _ = synth.make_inputs(S, Hq, Hkv, 128, seed=7, device="cuda")
+    out, res = sa.sample_attention(q, k, v, alpha=0.95, chunk_n=2)
+    m = res.mask
+    nb, G = m.n_qblocks, Hq // Hkv
+    order = m.order(G, 0).cpu().numpy().reshape(-1, 2)
+    cnt = m.kv_cnt.cpu().numpy()
+    grid = m.to_dense()
+    items = order[order >= 0]
+    assert np.array_equal(np.sort(items), np.arange(Hq * nb))
+    last = None
+    singles = 0
+    for a, b in order:
+        ha, qa = divmod(int(a), nb)
+        g = ha // G
+        if b >= 0:
+            hb, qbb = divmod(int(b), nb)
+            assert hb // G == g
+            assert qa == qbb or (ha == hb and ha % G == G - 1 and G % 2 == 1 and qbb == qa + 1)
+            singles += int((grid[ha, qa] ^ grid[hb, qbb]).sum())
+        c = cnt.flat[a] + (cnt.flat[b] if b >= 0 else 0)
+        if last is not None and last[0] == g:
+            assert c <= last[1]
+        last = (g, c)
+    fixed = sum(int((grid[g * G + 2 * p, qb] ^ grid[g * G + 2 * p + 1, qb]).sum())
+                for g in range(Hkv) for p in range(G // 2) for qb in range(nb))
+    fixed += sum(int((grid[g * G + G - 1, 2 * j] ^ grid[g * G + G - 1, 2 * j + 1]).sum())
+                 for g in range(Hkv) if G % 2 for j in range(nb // 2))
+    assert singles <= fixed
+    # the same mask through the natural (fixed) unit order gives the same output
+    b = sa.HeadBatch.from_tensors(q, k, v)
+    o2 = torch.empty_like(q)
+    st = torch.cuda.current_stream().cuda_stream
+    rc = _lib.load().sa_sparse_forward(q.data_ptr(), k.data_ptr(), v.data_ptr(), _lib.SA_BF16, S, Hq, Hkv, 128, 128,
+                                       b.group, 0, m.kv_cnt.data_ptr(), m.kv_idx.data_ptr(), None, o2.data_ptr(),
+                                       None, None, st)
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert torch.equal(out, o2)

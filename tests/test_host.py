@@ -118,4 +118,4 @@ def test_c_abi_rejects_bad_arguments_without_touching_the_gpu():
     assert rc == _lib.SA_ERR_UNSUPPORTED
     # the Python wrapper turns these codes into the reference's exception types
     with pytest.raises(sa.InputError):
-        _lib.call("sa_schedule", None, 1, 1, 1, 0, None, None)
+        _lib.call("sa_schedule", None, None, 1, 1, 1, 0, None, None, None)
