@@ -531,10 +531,11 @@ def e2e_run(sa, q, k, v, alpha, chunk_n, group, q_head0, args, dev, world, dense
                                        q_head0=q_head0, group=group)
             ho.copy_(o, non_blocking=True)
 
-    run()
+    for _ in range(2):  # warm-up: staging buffers, kernel attributes
+        run()
     torch.cuda.synchronize(dev)
     ts = []
-    for _ in range(max(1, min(args.steps, 3))):
+    for _ in range(max(1, min(args.steps, 5))):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         run()

@@ -84,6 +84,13 @@ size_t sa_workspace_bytes(int S, int Hq, int Hkv, int d, int blk, int chunk_n, i
  * to 1 (never cleared) when any of the n elements is NaN or Inf. */
 int sa_check_finite(const void* x, int dtype, int64_t n, int* flag_dev, void* stream);
 
+/* Host-side helper of the host-buffer entry point: `height` rows of `width`
+ * bytes from src (row pitch spitch) to dst (row pitch dpitch), host or device
+ * pointers, stream-ordered (cudaMemcpy2DAsync).  Moves the sampled query
+ * windows of every head in one copy engine transfer. */
+int sa_copy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                    void* stream);
+
 /* Stage 1 — replaces sample_scores + block_reduce (sampler.py:135-191) for
  * every q head and every chunk of the plan (plan_chunks, sampler.py:88-118:
  * window i samples rows [max(0, (i+1)*itv - blk), (i+1)*itv)).

@@ -189,6 +189,17 @@ int sa_check_finite(const void* x, int dtype, int64_t n, int* flag_dev, void* st
   return launch_check_finite(x, dtype, n, flag_dev, static_cast<cudaStream_t>(stream));
 }
 
+int sa_copy2d_async(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                    void* stream) {
+  if (!dst || !src) return fail(SA_ERR_INVALID, "sa_copy2d_async: null pointer");
+  if (width > dpitch || width > spitch) return fail(SA_ERR_INVALID, "sa_copy2d_async: width exceeds a pitch");
+  if (!width || !height) return SA_OK;
+  const cudaError_t e = cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault,
+                                          static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(SA_ERR_CUDA, std::string("sa_copy2d_async: ") + cudaGetErrorString(e));
+  return SA_OK;
+}
+
 int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, int d, int blk,
               int group, int q_head0, int chunk_n, int itv, double* col, double* slash,
               double* logit_bound, int mode, const int* only_flags, void* workspace,

@@ -5,9 +5,9 @@
 // re-score of (head, chunk) pairs whose tensor-core scores sit too close to a
 // find_k / arg_topk decision to trust (sa_select margin flags).
 //
-// Same single-pass structure as the tensor-core path, in fp64 on the SIMT
-// pipes: one CTA per (head, chunk, key-block split) scores the window's rows
-// against each key block (128 x 128 dot products, 8x8 fp64 register tiles),
+// Same single-pass structure as the tensor-core path, in fp64: one CTA per
+// (head, chunk, key-block split) scores the window's rows against each key
+// block (128 x 128 dot products on the FP64 tensor cores, mma.sync m8n8k4),
 // keeps a running per-row max m, and emits per (row, key block)
 //     A = sum_{t <= r % blk} exp(s - m),  B = sum_{t > r % blk} exp(s - m)
 // (causal keys only).  xf_rowfin / xf_fold then normalise with the rows'
@@ -25,19 +25,14 @@
 namespace sa {
 namespace {
 
-#ifndef SA_XF_DMMA
-#define SA_XF_DMMA 1  // FP64 tensor-core inner products (0: the SIMT 8x8 register-tile version)
-#endif
-#ifndef SA_XF_W16
-#define SA_XF_W16 1  // DMMA with 16 warps of one 8-row tile each (0: 8 warps of two tiles)
-#endif
-// SIMT: 16 x 16 threads, ty -> rows ty + 16a (a < 8), tx -> keys tx + 16b (b < 8).
-// DMMA: warp w -> rows kMT*8*w .. +kMT*8 (kMT 8-row tiles) x all 128 keys.
-constexpr int kThreads = (SA_XF_DMMA && SA_XF_W16) ? 512 : 256;
-constexpr int kMT = (SA_XF_DMMA && SA_XF_W16) ? 1 : 2;
+// 16 warps; warp w owns rows 8w..8w+7 of the window x all 128 keys of a block.
+constexpr int kThreads = 512;
 constexpr int kRows = 128;
 constexpr int kKeys = 128;
-constexpr int kDChunk = 64;    // head-dim slice staged per round
+constexpr int kDChunk = 32;      // head-dim slice of K staged per round (double-buffered)
+constexpr int kPitchQ = 132;     // fp64 smem pitches = 4 (mod 32): conflict-free m8n8k4 fragment loads
+constexpr int kPitchK = 36;
+constexpr int kXfSmemBytes = (kRows * kPitchQ + 2 * kKeys * kPitchK) * 8;
 
 struct Win {
   int ss, se, nkb;  // sampled rows [ss, se); key blocks 0..nkb-1 hold keys < se
@@ -63,18 +58,54 @@ __device__ __forceinline__ float to_f<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-// stage rows [r0, r0+n) x dims [c0, c0+kDChunk) of a row-major [*, d] matrix into smem [kRows][kDChunk+1]
-// (staged as fp64 so the inner product loop issues no conversions)
+// 8 consecutive elements of row r, dims [c, c+8), of a row-major [n, d]
+// matrix (zero past n rows / d dims); one 16-byte load per 8 bf16 (or two per
+// 8 floats) when d allows it.
 template <typename T>
-__device__ void stage(double* dst, const T* src, int n, int d, int c0) {
-  const int cn = min(kDChunk, d - c0);
-  for (int e = threadIdx.x; e < kRows * kDChunk; e += kThreads) {
-    const int r = e / kDChunk, c = e - r * kDChunk;
-    dst[r * (kDChunk + 1) + c] = (r < n && c < cn) ? (double)to_f(src[(size_t)r * d + c0 + c]) : 0.0;
+struct Oct {
+  double v[8];
+  __device__ __forceinline__ void load(const T* __restrict__ src, int r, int n, int c, int d) {
+    if (r >= n || c >= d) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.0;
+      return;
+    }
+    const T* p = src + (size_t)r * d + c;
+    if (c + 8 <= d && d % 8 == 0) {
+      if constexpr (sizeof(T) == 2) {
+        const uint4 u = *reinterpret_cast<const uint4*>(p);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          v[2 * i] = (double)__uint_as_float(w[i] << 16);
+          v[2 * i + 1] = (double)__uint_as_float(w[i] & 0xffff0000u);
+        }
+      } else {
+        const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+        v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+      }
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = c + i < d ? (double)to_f(p[i]) : 0.0;
   }
+  __device__ __forceinline__ void store(double* dst) const {
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) *reinterpret_cast<double2*>(dst + i) = make_double2(v[i], v[i + 1]);
+  }
+};
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
 }
 
-// Work of one CTA: key blocks [kb0, kb1) of (head, chunk) hc.
+// Work of one CTA: key blocks [kb0, kb1) of (head, chunk) hc.  The window's
+// query rows are staged once (fp64, all d dims); K streams through two
+// 32-dim smem buffers, the next slice's global loads issued into registers
+// before the current slice's MMAs so their latency hides under them.  Lane
+// (gq = lane / 4, tg = lane % 4) of warp w holds rows 8w + gq, keys 8nt + 2tg + {0, 1}.
 template <typename T>
 __device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __restrict__ k, const Stage1Geom& g,
                                         int hc, int kb0, int kb1, double* __restrict__ pa,
@@ -83,190 +114,96 @@ __device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __rest
   const int h = hc / g.cn, c = hc - h * g.cn;
   const Win w = window_of(c, g.S, g.blk, g.itv);
   kb1 = min(kb1, w.nkb);
-  const int kvh = kv_head_of(h, g.group, g.q_head0);
-  const int nr = w.se - w.ss, d = g.d, blk = g.blk;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const T* qh = q + ((size_t)h * g.S + w.ss) * d;
-  const T* kh = k + (size_t)kvh * g.S * d;
-  const double scale = 1.0 / sqrt((double)d);
-  double m_run[8];
-#pragma unroll
-  for (int a = 0; a < 8; ++a) m_run[a] = -INFINITY;
-
-  for (int kb = kb0; kb < kb1; ++kb) {
-    const int key0 = kb * blk;
-    const int nk = min(blk, w.se - key0);  // keys of this block that any sampled row can see
-    double acc[8][8];
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-      for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
-    for (int c0 = 0; c0 < d; c0 += kDChunk) {
-      __syncthreads();
-      stage(qs, qh, nr, d, c0);
-      stage(ks, kh + (size_t)key0 * d, nk, d, c0);
-      __syncthreads();
-      const int cn = min(kDChunk, d - c0);
-      for (int i = 0; i < cn; ++i) {
-        double qv[8], kv[8];
-#pragma unroll
-        for (int a = 0; a < 8; ++a) qv[a] = qs[(ty + 16 * a) * (kDChunk + 1) + i];
-#pragma unroll
-        for (int b = 0; b < 8; ++b) kv[b] = ks[(tx + 16 * b) * (kDChunk + 1) + i];
-#pragma unroll
-        for (int a = 0; a < 8; ++a)
-#pragma unroll
-          for (int b = 0; b < 8; ++b) acc[a][b] = fma(qv[a], kv[b], acc[a][b]);
-      }
-    }
-    // per row: block max over causal keys (16 tx lanes of the warp share a row set)
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      const int rl = ty + 16 * a;
-      const int row = w.ss + rl;
-      double mx = -INFINITY;
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const int t = tx + 16 * b;
-        acc[a][b] *= scale;
-        if (t < nk && key0 + t <= row) mx = fmax(mx, acc[a][b]);
-      }
-#pragma unroll
-      for (int o = 1; o < 16; o <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const double m_new = fmax(m_run[a], mx);
-      const int rho = row % blk;
-      double sa_ = 0.0, sb_ = 0.0;
-      if (m_new != -INFINITY) {
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          const int t = tx + 16 * b;
-          if (t < nk && key0 + t <= row) {
-            const double p = exp(acc[a][b] - m_new);
-            if (t <= rho) sa_ += p; else sb_ += p;
-          }
-        }
-      }
-#pragma unroll
-      for (int o = 1; o < 16; o <<= 1) {
-        sa_ += __shfl_xor_sync(0xffffffffu, sa_, o);
-        sb_ += __shfl_xor_sync(0xffffffffu, sb_, o);
-      }
-      m_run[a] = m_new;
-      if (tx == 0 && rl < nr) {
-        const size_t o = ((size_t)hc * blk + rl) * g.nb + kb;
-        pa[o] = sa_;
-        pb[o] = sb_;
-        pm[o] = m_new;
-      }
-    }
-  }
-}
-
-
-constexpr int kPitchD = 68;  // DMMA staging pitch (doubles): conflict-free fragment loads
-
-template <typename T>
-__device__ void stage_p(double* dst, const T* src, int n, int d, int c0) {
-  const int cn = min(kDChunk, d - c0);
-  for (int e = threadIdx.x; e < kRows * kDChunk; e += kThreads) {
-    const int r = e / kDChunk, c = e - r * kDChunk;
-    dst[r * kPitchD + c] = (r < n && c < cn) ? (double)to_f(src[(size_t)r * d + c0 + c]) : 0.0;
-  }
-}
-
-__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-
-// xf_work on the FP64 tensor cores (mma.sync m8n8k4): warp w owns rows
-// 16w..16w+15 (two 8-row tiles) x all 128 keys (sixteen 8-key tiles); lane
-// (g = lane / 4, c = lane % 4) holds rows 16w + 8mt + g, keys 8nt + 2c + {0, 1}.
-template <typename T>
-__device__ __forceinline__ void xf_work_dmma(const T* __restrict__ q, const T* __restrict__ k, const Stage1Geom& g,
-                                             int hc, int kb0, int kb1, double* __restrict__ pa,
-                                             double* __restrict__ pb, double* __restrict__ pm, double* qs,
-                                             double* ks) {
-  const int h = hc / g.cn, c = hc - h * g.cn;
-  const Win w = window_of(c, g.S, g.blk, g.itv);
-  kb1 = min(kb1, w.nkb);
+  if (kb0 >= kb1) return;
   const int kvh = kv_head_of(h, g.group, g.q_head0);
   const int nr = w.se - w.ss, d = g.d, blk = g.blk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tg = lane & 3;
   const T* qh = q + ((size_t)h * g.S + w.ss) * d;
   const T* kh = k + (size_t)kvh * g.S * d;
   const double scale = 1.0 / sqrt((double)d);
-  double m_run[kMT];
-#pragma unroll
-  for (int mt = 0; mt < kMT; ++mt) m_run[mt] = -INFINITY;
+  const int nch = (d + kDChunk - 1) / kDChunk;  // K slices per key block
+  // staging map: thread -> (row, 8 dims) of a 128 x 32 slice
+  const int sr = threadIdx.x >> 2, sc = (threadIdx.x & 3) * 8;
+  for (int e = threadIdx.x; e < kRows * (kPitchQ / 8); e += kThreads) {  // Q once, all dims
+    const int r = e / (kPitchQ / 8), c8 = (e - r * (kPitchQ / 8)) * 8;
+    if (c8 + 8 > kPitchQ) continue;
+    Oct<T> o;
+    o.load(qh, r, nr, c8, d);
+    o.store(qs + r * kPitchQ + c8);
+  }
+  auto nk_of = [&](int kb) { return min(blk, w.se - kb * blk); };  // keys any sampled row can see
+  Oct<T> nxt;
+  nxt.load(kh + (size_t)kb0 * blk * d, sr, nk_of(kb0), sc, d);
+  nxt.store(ks + sr * kPitchK + sc);
+  __syncthreads();
+  double m_run = -INFINITY;
+  int buf = 0;
   for (int kb = kb0; kb < kb1; ++kb) {
     const int key0 = kb * blk;
-    const int nk = min(blk, w.se - key0);
-    double acc[kMT][16][2];
+    const int nk = nk_of(kb);
+    double acc[16][2];
 #pragma unroll
-    for (int mt = 0; mt < kMT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 16; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    for (int c0 = 0; c0 < d; c0 += kDChunk) {
-      __syncthreads();
-      stage_p(qs, qh, nr, d, c0);
-      stage_p(ks, kh + (size_t)key0 * d, nk, d, c0);
-      __syncthreads();
-      const int cn = min(kDChunk, d - c0);
-      for (int kc = 0; kc < cn; kc += 4) {
-        double a[kMT], b[16];
-#pragma unroll
-        for (int mt = 0; mt < kMT; ++mt) a[mt] = qs[(8 * kMT * warp + 8 * mt + gq) * kPitchD + kc + tg];
-#pragma unroll
-        for (int nt = 0; nt < 16; ++nt) b[nt] = ks[(8 * nt + gq) * kPitchD + kc + tg];
-#pragma unroll
-        for (int mt = 0; mt < kMT; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 16; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+    for (int nt = 0; nt < 16; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+    for (int ch = 0; ch < nch; ++ch) {
+      // prefetch the next slice (this block's next 32 dims, or the next block's first)
+      const bool more = ch + 1 < nch || kb + 1 < kb1;
+      if (more) {
+        const int kbn = ch + 1 < nch ? kb : kb + 1, chn = ch + 1 < nch ? ch + 1 : 0;
+        nxt.load(kh + (size_t)kbn * blk * d, sr, nk_of(kbn), chn * kDChunk + sc, d);
       }
-    }
+      const double* kq = ks + buf * (kKeys * kPitchK);
+      const double* qq = qs + (8 * warp + gq) * kPitchQ + ch * kDChunk + tg;
 #pragma unroll
-    for (int mt = 0; mt < kMT; ++mt) {
-      const int rl = 8 * kMT * warp + 8 * mt + gq;
-      const int row = w.ss + rl;
-      double mx = -INFINITY;
+      for (int kc = 0; kc < kDChunk; kc += 4) {
+        const double a = qq[kc];
+        double b[16];
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt) b[nt] = kq[(8 * nt + gq) * kPitchK + kc + tg];
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt) dmma_8x8x4(acc[nt][0], acc[nt][1], a, b[nt]);
+      }
+      if (more) nxt.store(ks + (buf ^ 1) * (kKeys * kPitchK) + sr * kPitchK + sc);
+      buf ^= 1;
+      __syncthreads();
+    }
+    const int rl = 8 * warp + gq;
+    const int row = w.ss + rl;
+    double mx = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = 8 * nt + 2 * tg + e;
+        acc[nt][e] *= scale;
+        if (t < nk && key0 + t <= row) mx = fmax(mx, acc[nt][e]);
+      }
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const double m_new = fmax(m_run, mx);
+    const int rho = row % blk;
+    double sa_ = 0.0, sb_ = 0.0;
+    if (m_new != -INFINITY) {
 #pragma unroll
       for (int nt = 0; nt < 16; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int t = 8 * nt + 2 * tg + e;
-          acc[mt][nt][e] *= scale;
-          if (t < nk && key0 + t <= row) mx = fmax(mx, acc[mt][nt][e]);
-        }
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      const double m_new = fmax(m_run[mt], mx);
-      const int rho = row % blk;
-      double sa_ = 0.0, sb_ = 0.0;
-      if (m_new != -INFINITY) {
-#pragma unroll
-        for (int nt = 0; nt < 16; ++nt)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int t = 8 * nt + 2 * tg + e;
-            if (t < nk && key0 + t <= row) {
-              const double p = exp(acc[mt][nt][e] - m_new);
-              if (t <= rho) sa_ += p; else sb_ += p;
-            }
+          if (t < nk && key0 + t <= row) {
+            const double p = exp(acc[nt][e] - m_new);
+            if (t <= rho) sa_ += p; else sb_ += p;
           }
-      }
-      sa_ += __shfl_xor_sync(0xffffffffu, sa_, 1);
-      sb_ += __shfl_xor_sync(0xffffffffu, sb_, 1);
-      sa_ += __shfl_xor_sync(0xffffffffu, sa_, 2);
-      sb_ += __shfl_xor_sync(0xffffffffu, sb_, 2);
-      m_run[mt] = m_new;
-      if (tg == 0 && rl < nr) {
-        const size_t o = ((size_t)hc * blk + rl) * g.nb + kb;
-        pa[o] = sa_;
-        pb[o] = sb_;
-        pm[o] = m_new;
-      }
+        }
+    }
+    sa_ += __shfl_xor_sync(0xffffffffu, sa_, 1);
+    sb_ += __shfl_xor_sync(0xffffffffu, sb_, 1);
+    sa_ += __shfl_xor_sync(0xffffffffu, sa_, 2);
+    sb_ += __shfl_xor_sync(0xffffffffu, sb_, 2);
+    m_run = m_new;
+    if (tg == 0 && rl < nr) {
+      const size_t o = ((size_t)hc * blk + rl) * g.nb + kb;
+      pa[o] = sa_;
+      pb[o] = sb_;
+      pm[o] = m_new;
     }
   }
 }
@@ -279,17 +216,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     xf_pass(const T* __restrict__ q, const T* __restrict__ k, Stage1Geom g, const int* __restrict__ list,
             int kb_per_cta, double* __restrict__ pa, double* __restrict__ pb, double* __restrict__ pm) {
   extern __shared__ double smem_d[];
-  double* qs = smem_d;                                              // [kRows][pitch]
-  double* ks = smem_d + kRows * (SA_XF_DMMA ? kPitchD : kDChunk + 1);  // [kKeys][pitch]
+  double* qs = smem_d;                    // [kRows][kPitchQ]
+  double* ks = smem_d + kRows * kPitchQ;  // 2 x [kKeys][kPitchK]
   const int n_pairs = list ? list[0] : g.Hq * g.cn;
   const int kb0 = blockIdx.x * kb_per_cta;
   for (int f = blockIdx.y; f < n_pairs; f += gridDim.y) {  // uniform per CTA
     const int hc = list ? list[1 + f] : f;
-#if SA_XF_DMMA
-    xf_work_dmma(q, k, g, hc, kb0, kb0 + kb_per_cta, pa, pb, pm, qs, ks);
-#else
     xf_work(q, k, g, hc, kb0, kb0 + kb_per_cta, pa, pb, pm, qs, ks);
-#endif
     __syncthreads();  // qs / ks are reused by the next pair
   }
 }
@@ -337,12 +270,19 @@ __global__ void s1_rowfin(Stage1Geom g, const int* __restrict__ list, const TPla
 }
 
 // Per key block: fold the rows' normalised partial masses into part3
-// (col, slash X-1, X, X+1).  Thread per key block, rows in a fixed order.
+// (col, slash X-1, X, X+1).  A CTA covers 32 key blocks of one pair with 8
+// row groups of 16 rows (256 threads: lanes = key blocks, so every row's loads
+// are coalesced); each thread folds its rows in order and the 8 partial sums
+// are added in group order, so the result is deterministic.  (A thread per
+// key block looping over all 128 rows left the fold latency-bound: ~140 us
+// at C3 for 50 MB.)
+constexpr int kFoldKb = 32, kFoldGroups = 8;
+
 template <typename TPlane, bool kLog2>
 __device__ __forceinline__ void fold_pair(Stage1Geom g, int hc, const TPlane* __restrict__ pa,
                                           const TPlane* __restrict__ pb, const TPlane* __restrict__ pm,
                                           const double* __restrict__ rowstat, double* __restrict__ part3,
-                                          double (*s_w)[2]) {
+                                          double (*s_w)[2], double (*s_acc)[kFoldKb][4]) {
   const Win w = window_of(hc % g.cn, g.S, g.blk, g.itv);
   const int nr = w.se - w.ss;
   for (int r = threadIdx.x; r < nr; r += blockDim.x) {
@@ -350,41 +290,51 @@ __device__ __forceinline__ void fold_pair(Stage1Geom g, int hc, const TPlane* __
     s_w[r][1] = 1.0 / rowstat[((size_t)hc * g.blk + r) * 2 + 1];
   }
   __syncthreads();
-  const int kb = blockIdx.x * blockDim.x + threadIdx.x;
-  if (kb >= g.nb) return;
-  double* out = part3 + ((size_t)hc * g.nb + kb) * 4;
-  if (kb >= w.nkb) {
-    out[0] = out[1] = out[2] = out[3] = 0.0;
-    return;
-  }
+  const int lane = threadIdx.x % kFoldKb, grp = threadIdx.x / kFoldKb;
+  const int kb = blockIdx.x * kFoldKb + lane;
   const int b0 = w.ss / g.blk;
+  const int per = (g.blk + kFoldGroups - 1) / kFoldGroups;
   double s4[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int r = 0; r < nr; ++r) {
-    const size_t o = ((size_t)hc * g.blk + r) * g.nb + kb;
-    const double m = (double)pm[o];
-    if (m == -INFINITY) continue;
-    const double wgt = (kLog2 ? exp2(m - s_w[r][0]) : exp(m - s_w[r][0])) * s_w[r][1];
-    const double a = (double)pa[o] * wgt, b = (double)pb[o] * wgt;
-    const int slot_a = (w.ss + r) / g.blk - b0 + 1;  // bin r//blk - kb, relative to X-1
-    s4[0] += a + b;
-    s4[1 + slot_a] += a;
-    s4[slot_a] += b;  // bin r//blk - kb - 1
+  if (kb < w.nkb) {
+    const int r1 = min(nr, (grp + 1) * per);
+    for (int r = grp * per; r < r1; ++r) {
+      const size_t o = ((size_t)hc * g.blk + r) * g.nb + kb;
+      const double m = (double)pm[o];
+      if (m == -INFINITY) continue;
+      const double wgt = (kLog2 ? exp2(m - s_w[r][0]) : exp(m - s_w[r][0])) * s_w[r][1];
+      const double a = (double)pa[o] * wgt, b = (double)pb[o] * wgt;
+      const int slot_a = (w.ss + r) / g.blk - b0 + 1;  // bin r//blk - kb, relative to X-1
+      s4[0] += a + b;
+      s4[1 + slot_a] += a;
+      s4[slot_a] += b;  // bin r//blk - kb - 1
+    }
   }
-  out[0] = s4[0];
-  out[1] = s4[1];
-  out[2] = s4[2];
-  out[3] = s4[3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s_acc[grp][lane][i] = s4[i];
+  __syncthreads();
+  if (grp == 0 && kb < g.nb) {
+    double t4[4] = {0.0, 0.0, 0.0, 0.0};
+    if (kb < w.nkb)
+      for (int x = 0; x < kFoldGroups; ++x)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t4[i] += s_acc[x][lane][i];
+    double* out = part3 + ((size_t)hc * g.nb + kb) * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = t4[i];
+  }
 }
 
 template <typename TPlane, bool kLog2>
-__global__ void s1_fold(Stage1Geom g, const int* __restrict__ list, const TPlane* __restrict__ pa,
-                        const TPlane* __restrict__ pb, const TPlane* __restrict__ pm,
-                        const double* __restrict__ rowstat, double* __restrict__ part3) {
-  __shared__ double s_w[kMaxSimtBlk][2];  // (M, 1/L) per row
+__global__ void __launch_bounds__(kFoldKb * kFoldGroups)
+    s1_fold(Stage1Geom g, const int* __restrict__ list, const TPlane* __restrict__ pa,
+            const TPlane* __restrict__ pb, const TPlane* __restrict__ pm,
+            const double* __restrict__ rowstat, double* __restrict__ part3) {
+  __shared__ double s_w[kMaxSimtBlk][2];                  // (M, 1/L) per row
+  __shared__ double s_acc[kFoldGroups][kFoldKb][4];       // per row group
   const int n_pairs = list ? list[0] : g.Hq * g.cn;
   for (int f = blockIdx.y; f < n_pairs; f += gridDim.y) {
-    fold_pair<TPlane, kLog2>(g, list ? list[1 + f] : f, pa, pb, pm, rowstat, part3, s_w);
-    __syncthreads();  // s_w is reloaded for the next pair
+    fold_pair<TPlane, kLog2>(g, list ? list[1 + f] : f, pa, pb, pm, rowstat, part3, s_w, s_acc);
+    __syncthreads();  // s_w / s_acc are reloaded for the next pair
   }
 }
 
@@ -445,7 +395,8 @@ int launch_fold(const Stage1Geom& g, const int* only, const TPlane* pa, const TP
   }
   s1_rowfin<TPlane, kLog2><<<dim3(16, rows), 256, 0, st>>>(g, list, pa, pb, pm, rowstat);
   if (int e = check_launch("stage1 rowfin")) return e;
-  s1_fold<TPlane, kLog2><<<dim3(ceil_div(g.nb, 128), rows), 128, 0, st>>>(g, list, pa, pb, pm, rowstat, part3);
+  s1_fold<TPlane, kLog2><<<dim3(ceil_div(g.nb, kFoldKb), rows), kFoldKb * kFoldGroups, 0, st>>>(
+      g, list, pa, pb, pm, rowstat, part3);
   if (int e = check_launch("stage1 fold")) return e;
   s1_finalize<<<only ? n_all : n_all, 256, 0, st>>>(g, list, part3, col, slash);
   return check_launch("stage1 finalize");
@@ -514,14 +465,16 @@ namespace {
 template <typename T>
 int run_exact(const Stage1Geom& g, const T* q, const T* k, const int* only, char* ws, const Workspace& L,
               double* col, double* slash, cudaStream_t st) {
-  const size_t smem = (size_t)(kRows + kKeys) * (SA_XF_DMMA ? kPitchD : kDChunk + 1) * sizeof(double);
+  const size_t smem = kXfSmemBytes;
   set_smem_attr(reinterpret_cast<const void*>(&xf_pass<T>), (int)smem);
   const size_t plane = (size_t)g.Hq * g.cn * g.blk * g.nb;
   double* pa = reinterpret_cast<double*>(ws + L.x_part);
   double* pb = pa + plane;
   double* pm = pb + plane;
+  // key blocks per CTA: Q is staged once per CTA, so longer runs amortise it;
+  // the flagged-pair grid (few pairs) keeps ~4+ waves on the SMs
   const long long work = (long long)g.Hq * g.cn * g.nb;
-  const int kpc = only ? 1 : (int)std::max<long long>(2, std::min<long long>(32, work / (148LL * 4)));
+  const int kpc = only ? 8 : (int)std::max<long long>(2, std::min<long long>(32, work / (148LL * 4)));
   const int n_all = g.Hq * g.cn;
   int* list = nullptr;
   if (only) {

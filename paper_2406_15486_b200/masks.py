@@ -82,7 +82,11 @@ class BlockMask:
         return self.kv_cnt.device
 
     def head(self, h: int) -> "BlockMask":
-        sl = slice(h, h + 1)
+        return self.heads(h, h + 1)
+
+    def heads(self, h0: int, h1: int) -> "BlockMask":
+        """The mask of heads [h0, h1) (views of the same device arrays)."""
+        sl = slice(h0, h1)
         return BlockMask(self.blk, self.S, self.kv_cnt[sl], self.kv_idx[sl],
                          None if self.k_sel is None else self.k_sel[sl],
                          None if self.idx_sel is None else self.idx_sel[sl],

@@ -3,26 +3,33 @@ host memory, with the PCIe transfers overlapped with the kernels.
 
 The reference is called with host arrays (numpy heads, pkg/src/blocksift/
 pipeline.py:149), so a drop-in has to move 1.1 GB of q/k/v in and 1 GB of
-output out at 128K x 32 heads.  Done naively (copy in, compute, copy out)
-the copies cost more than the attention itself.  Here the q heads are split
-into groups inside their KV group; all host->device copies are queued up
-front on one copy stream (each KV head ahead of its first q group), each
-group's three stages run on the compute stream as soon as its inputs land,
-and its output goes back on a second copy stream while the next group
-computes.  The result is the same as sample_attention on the whole batch:
-stages 1-3 are independent per q head (ref pipeline.py:169).
+output out at 128K x 32 heads, ~40 ms of PCIe against ~36 ms of kernels.
+Stages 1 and 2 read only K and the SAMPLED query windows (128 rows per chunk,
+ref sampler.py:103-117), so the copy stream sends K/V and those windows
+first (~2 % of the bytes); stages 1-2 then run for ALL heads at once while
+the bulk of Q streams in behind them.  Stage 3 runs per head group as each
+group's Q lands (one launch per group; the groups shrink at the end so the
+last device->host copy is short), and each group's output goes back on a
+second copy stream while the next group computes.  The result is that of
+sample_attention on the whole batch: stages 1-3 are independent per q head
+(ref pipeline.py:169) and stage 3 of a head reads only that head's rows.
 """
 
 from __future__ import annotations
 
+import contextlib
+import threading
+
 import numpy as np
 import torch
 
+from .config import plan_chunks, resolve_config
 from .errors import InputError
-from .heads import check_finite_async, raise_on_flags
-from .pipeline import sample_attention
+from .heads import HeadBatch, check_finite_async, dcall, raise_on_flags
+from .pipeline import SampleAttentionResult
+from .stages import block_reduce, merge_index, sample_scores, select, sparse_attention
 
-__all__ = ["sample_attention_host"]
+__all__ = ["sample_attention_host", "release_staging"]
 
 
 def _as_host(x) -> torch.Tensor:
@@ -34,106 +41,172 @@ def _as_host(x) -> torch.Tensor:
 
 
 def _group_plan(Hq: int, group: int, hpg: int) -> list:
-    """Head groups [h0, h1) inside KV-group boundaries.  The first groups of
-    the batch are small (1, then 2 heads) so the first kernels start after a
-    short copy, and the last groups shrink again (2, then 1) so the final
-    device->host copy after the last kernel is short; the rest use `hpg`."""
-    sizes_per_kv = []
+    """Stage-3 head groups [h0, h1) inside KV-group boundaries.  A head's Q
+    crosses PCIe in ~0.6x the time its stage 3 takes (128K), so the groups
+    ramp up (2, 3, 5 heads, then `hpg`): each group's copy hides under the
+    previous group's kernels.  The last groups shrink (3, 2, then 1 head):
+    each group's output copy hides under the next group's kernels and the
+    copy after the last kernel is short."""
+    groups, h0 = [], 0
     n_kv = Hq // group
     for g in range(n_kv):
-        head, tail = [], []
-        rest = group
-        if g == 0:
-            for s in (1, 2):
-                if rest > s:
-                    head.append(s)
-                    rest -= s
+        rest, head, tail = group, [], []
         if g == n_kv - 1:
-            for s in (1, 2):
+            for s in (1, 2, 3):
                 if rest > s:
                     tail.insert(0, s)
                     rest -= s
-        n_mid = -(-rest // hpg)  # near-equal middle groups of at most hpg heads
-        mid = [rest // n_mid + (1 if i < rest % n_mid else 0) for i in range(n_mid)] if rest else []
-        sizes_per_kv.append(head + mid + tail)
-    groups, h0 = [], 0
-    for sizes in sizes_per_kv:
+        if g == 0:
+            for s in (2, 3, 5):
+                if rest > s:
+                    head.append(s)
+                    rest -= s
+        n_mid = -(-rest // hpg)  # near-equal groups of at most hpg heads
+        sizes = head + ([rest // n_mid + (1 if i < rest % n_mid else 0) for i in range(n_mid)] if rest else []) + tail
         for s in sizes:
             groups.append((h0, h0 + s))
             h0 += s
     return groups
 
 
-def sample_attention_host(q, k, v, heads_per_group: int = 4, device=None, out: torch.Tensor | None = None,
-                          check_inputs: bool = True, dtype=torch.bfloat16, **kw):
+def sample_attention_host(q, k, v, heads_per_group: int = 8, device=None, out: torch.Tensor | None = None,
+                          check_inputs: bool = True, dtype=torch.bfloat16, alpha: float = 0.95,
+                          alpha_c: float | None = None, alpha_s: float | None = None, chunk_n: int | None = None,
+                          sample_ratio: float | None = None, blk: int = 128, sink_blocks: int = 0,
+                          local_blocks: int = 1, guard: str = "auto", _lanes: int = 2):
     """q [Hq,S,d], k/v [Hkv,S,d] on the host -> (out [Hq,S,d] on the host,
-    list of per-group SampleAttentionResult).  Keyword arguments are those of
-    sample_attention (alpha, chunk_n / sample_ratio, guard, ...).
+    [SampleAttentionResult]).  Keyword arguments are those of sample_attention.
 
     For the transfers to overlap, pass pinned tensors (torch .pin_memory());
     pageable inputs are staged through pinned buffers first."""
     q, k, v = _as_host(q), _as_host(k), _as_host(v)
     if q.dim() != 3 or k.dim() != 3 or k.shape != v.shape or q.shape[1:] != k.shape[1:]:
         raise InputError(f"expected q [Hq,S,d] and k, v [Hkv,S,d]; got {tuple(q.shape)}, {tuple(k.shape)}")
-    Hq, Hkv = q.shape[0], k.shape[0]
+    Hq, Hkv, S = q.shape[0], k.shape[0], q.shape[1]
     if Hq % Hkv:
         raise InputError(f"Hq={Hq} is not a multiple of Hkv={Hkv}")
     group = Hq // Hkv
     hpg = max(1, min(heads_per_group, group))
-    while group % hpg:
-        hpg -= 1
+    cfg = resolve_config(S, alpha, alpha_c, alpha_s, chunk_n, sample_ratio, blk)
+    plan = plan_chunks(S, cfg)
     dev = torch.device(device or "cuda")
     if q.dtype != dtype:
         q, k, v = (t.to(dtype) for t in (q, k, v))
     if not q.is_pinned():
         q, k, v = (t.pin_memory() for t in (q, k, v))
-    dq = torch.empty(q.shape, dtype=dtype, device=dev)
-    dk = torch.empty(k.shape, dtype=dtype, device=dev)
-    dv = torch.empty(v.shape, dtype=dtype, device=dev)
-    dout = torch.empty_like(dq)
     if out is None:
         out = torch.empty(q.shape, dtype=dtype, pin_memory=True)
+    with _staging(dev, tuple(q.shape), tuple(k.shape), dtype) as st_:
+        return _run(q, k, v, out, st_, dev, group, hpg, cfg, plan, check_inputs, sink_blocks, local_blocks,
+                    guard, _lanes)
+
+
+class _Staging:
+    """Device copies of q/k/v/out and the copy / side streams of one geometry,
+    kept across calls: allocating 2+ GB per call costs the caching allocator
+    fresh cudaMallocs (up to ~17 ms measured at C3) whenever its blocks are
+    still tied to the previous call's streams."""
+
+    def __init__(self, dev, qshape, kshape, dtype):
+        self.dq = torch.empty(qshape, dtype=dtype, device=dev)
+        self.dk = torch.empty(kshape, dtype=dtype, device=dev)
+        self.dv = torch.empty(kshape, dtype=dtype, device=dev)
+        self.dout = torch.empty_like(self.dq)
+        self.h2d = torch.cuda.Stream(device=dev)
+        self.d2h = torch.cuda.Stream(device=dev)
+        self.side = torch.cuda.Stream(device=dev)
+        self.lock = threading.Lock()
+
+
+_STAGING: dict = {}
+_STAGING_LOCK = threading.Lock()
+
+
+@contextlib.contextmanager
+def _staging(dev, qshape, kshape, dtype):
+    key = (dev, qshape, kshape, dtype)
+    with _STAGING_LOCK:
+        st_ = _STAGING.get(key)
+        if st_ is None:
+            _STAGING.clear()  # one geometry at a time: the buffers are large
+            st_ = _STAGING[key] = _Staging(dev, qshape, kshape, dtype)
+    with st_.lock:
+        yield st_
+
+
+def release_staging() -> None:
+    """Free the cached device buffers of sample_attention_host."""
+    with _STAGING_LOCK:
+        _STAGING.clear()
+
+
+def _run(q, k, v, out, st_, dev, group, hpg, cfg, plan, check_inputs, sink_blocks, local_blocks, guard, _lanes):
+    Hq, S = q.shape[0], q.shape[1]
+    dq, dk, dv, dout = st_.dq, st_.dk, st_.dv, st_.dout
     compute = torch.cuda.current_stream(dev)
-    h2d = torch.cuda.Stream(device=dev)
-    d2h = torch.cuda.Stream(device=dev)
-    h2d.wait_stream(compute)  # dq/dk/dv were allocated on the compute stream
+    h2d, d2h, side = st_.h2d, st_.d2h, st_.side
+    h2d.wait_stream(compute)  # the previous call's readers of dq/dk/dv and this call's inputs
     groups = _group_plan(Hq, group, hpg)
-    ready = []
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    ready = []
+    # the copy stream carries copies only: a kernel queued on it (the NaN/Inf
+    # scan) would wait for SMs behind a running stage-3 launch and hold up
+    # every copy behind it
+    row_bytes = q.shape[2] * q.element_size()
     with torch.cuda.stream(h2d):
-        copied_kv = set()
-        for h0, h1 in groups:
-            kv = h0 // group
-            fresh = []
-            if kv not in copied_kv:
-                dk[kv].copy_(k[kv], non_blocking=True)
-                dv[kv].copy_(v[kv], non_blocking=True)
-                copied_kv.add(kv)
-                fresh = [dk[kv], dv[kv]]
+        # K (stage 1 reads every key) and the sampled query windows of every head, then V
+        dk.copy_(k, non_blocking=True)
+        for c in plan.chunks:
+            off = c.sample_start * row_bytes
+            dcall(dev, "sa_copy2d_async", dq.data_ptr() + off, S * row_bytes, q.data_ptr() + off, S * row_bytes,
+                  (c.sample_end - c.sample_start) * row_bytes, Hq, h2d.cuda_stream)
+        sampled = torch.cuda.Event()
+        sampled.record(h2d)
+        dv.copy_(v, non_blocking=True)
+        for h0, h1 in groups:  # the rest of Q, group by group (the windows are sent again; same bits)
             dq[h0:h1].copy_(q[h0:h1], non_blocking=True)
-            if check_inputs:  # the reference's NaN/Inf check (core.py:30-37), read once at the end
-                check_finite_async([dq[h0:h1]] + fresh, flag, h2d.cuda_stream)
             ev = torch.cuda.Event()
             ev.record(h2d)
             ready.append(ev)
-    results = []
-    for (h0, h1), ev in zip(groups, ready):
-        compute.wait_event(ev)
-        kv = h0 // group
-        _, res = sample_attention(dq[h0:h1], dk[kv:kv + 1], dv[kv:kv + 1], q_head0=h0, group=group,
-                                  out=dout[h0:h1], check_inputs=False, **kw)
-        results.append(res)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    compute.wait_event(sampled)
+    ev[0].record(compute)
+    if check_inputs:  # the reference's NaN/Inf check (core.py:30-37), read once at the end
+        check_finite_async([dk], flag, compute.cuda_stream)
+    batch = HeadBatch.from_tensors(dq, dk, dv, group=group)
+    reduced = block_reduce(sample_scores(batch, plan), cfg.blk)
+    ev[1].record(compute)
+    sel = select(reduced, cfg, guard=guard)
+    mask = merge_index(sel, plan, cfg.blk, S, sink_blocks, local_blocks)
+    ev[2].record(compute)
+    # stage-3 launches alternate between two streams, so a group's kernel fills
+    # the SMs the previous group's last wave leaves idle
+    side.wait_stream(compute)
+    lanes = (compute, side)
+    for i, ((h0, h1), landed) in enumerate(zip(groups, ready)):
+        st = lanes[i % _lanes]
+        st.wait_event(landed)
+        if check_inputs:
+            if i == 0:
+                check_finite_async([dv], flag, st.cuda_stream)
+            check_finite_async([dq[h0:h1]], flag, st.cuda_stream)
+        kv0, kv1 = h0 // group, (h1 - 1) // group + 1
+        with torch.cuda.stream(st):
+            part = HeadBatch.from_tensors(dq[h0:h1], dk[kv0:kv1], dv[kv0:kv1], group=group, q_head0=h0)
+            sparse_attention(part, mask.heads(h0, h1), out=dout[h0:h1], report=False)
         done = torch.cuda.Event()
-        done.record(compute)
+        done.record(st)
         d2h.wait_event(done)
         with torch.cuda.stream(d2h):
             out[h0:h1].copy_(dout[h0:h1], non_blocking=True)
+    compute.wait_stream(side)
+    ev[3].record(compute)
     compute.wait_stream(d2h)
-    for t in (dq, dk, dv, dout, flag):
-        t.record_stream(h2d)
-        t.record_stream(d2h)
+    flag.record_stream(side)
+    for t in (mask.kv_cnt, mask.kv_idx):
+        t.record_stream(side)
     # `out` is host memory: the caller may read it as soon as we return
     d2h.synchronize()
     if check_inputs:
         raise_on_flags(flag, dev)
-    return out, results
+    return out, [SampleAttentionResult(cfg, plan, mask, sel.flags, ev, None)]
