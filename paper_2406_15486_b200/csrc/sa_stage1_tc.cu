@@ -229,22 +229,39 @@ __global__ void __launch_bounds__(kThreads, 2)
 // the guard margin of a (head, chunk) is scaled by
 //   bound = max_{sampled rows r} ||q_r|| * max_{keys j} ||k_j|| / sqrt(d)
 // (Cauchy-Schwarz), so large-logit heads get a proportionally wider margin.
-// One warp per key row: max ||k_j||^2 per KV head (nonnegative floats order
-// like their bit patterns, so atomicMax on the bits is a float max).
+// Max ||k_j||^2 per KV head: 16 threads per key row (one 16-byte load each),
+// four rows in flight per half-warp so the loads overlap (nonnegative floats
+// order like their bit patterns, so atomicMax on the bits is a float max).
 __global__ void k_key_norm(const __nv_bfloat16* __restrict__ k, int S, unsigned* __restrict__ kmax2) {
   const int kvh = blockIdx.y;
-  const int lane = threadIdx.x & 31;
+  const int sub = threadIdx.x & 15;  // 16-byte slice of the row
+  const int half = (threadIdx.x >> 4) & 1;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // global warp: 8 rows per round
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const uint4* base = reinterpret_cast<const uint4*>(k + (size_t)kvh * S * 128);
   float best = 0.f;
-  for (int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < S; j += gridDim.x * (blockDim.x >> 5)) {
-    const uint2 u = __ldg(reinterpret_cast<const uint2*>(k + ((size_t)kvh * S + j) * 128) + lane);
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-    float ss = a.x * a.x + a.y * a.y + b.x * b.x + b.y * b.y;
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    best = fmaxf(best, ss);
+  for (int w0 = gw * 8; w0 < S; w0 += nw * 8) {  // warp-uniform trip count (the shuffles below)
+    const int j0 = w0 + half * 4;
+    uint4 u[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) u[r] = j0 + r < S ? __ldg(base + (size_t)(j0 + r) * 16 + sub) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t w[4] = {u[r].x, u[r].y, u[r].z, u[r].w};
+      float ss = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+        ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      best = fmaxf(best, ss);
+    }
   }
+  for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
   __shared__ float s_best[32];
-  if (lane == 0) s_best[threadIdx.x >> 5] = best;
+  if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = fmaxf(best, s_best[w]);
@@ -290,7 +307,7 @@ int launch_logit_bound(const Stage1Geom& g, const void* q, const void* k, char* 
                        double* bound, cudaStream_t st) {
   unsigned* kmax2 = reinterpret_cast<unsigned*>(ws + L.kmax2);
   cudaMemsetAsync(kmax2, 0, sizeof(unsigned) * g.Hkv, st);
-  const int per_kv = std::max(1, std::min(ceil_div(g.S, 8), 2 * 148 / std::max(1, g.Hkv) + 1));
+  const int per_kv = std::max(1, std::min(ceil_div(g.S, 64), 4 * 148 / std::max(1, g.Hkv) + 1));
   k_key_norm<<<dim3(per_kv, g.Hkv), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(k), g.S, kmax2);
   if (int e = check_launch("stage1 key norms")) return e;
   k_pair_bound<<<g.Hq * g.cn, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(q), g, kmax2, bound);

@@ -73,17 +73,21 @@ __global__ void __launch_bounds__(kSelThreads)
       __syncthreads();
     }
   }
-  // sequential fp64 cumulative sum in sorted order (np.cumsum semantics)
+  // sequential fp64 cumulative sum in sorted order (np.cumsum semantics): one
+  // thread, 32 scores loaded ahead per round so only the dependent adds are
+  // serial (adding the +0.0 tail leaves the sum bit-identical)
   if (threadIdx.x == 0) {
     double acc = 0.0;
-    int i = 0;
-    for (; i < nb; ++i) {
-      const unsigned long long kk = key[i];
-      if (kk == 0ull) break;  // the zero tail leaves the sum unchanged
-      acc += __longlong_as_double((long long)kk);
-      cum[i] = acc;
+    for (int i0 = 0; i0 < nb; i0 += 32) {
+      double v[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) v[t] = i0 + t < nb ? __longlong_as_double((long long)key[i0 + t]) : 0.0;
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        acc += v[t];
+        if (i0 + t < nb) cum[i0 + t] = acc;
+      }
     }
-    for (; i < nb; ++i) cum[i] = acc;
   }
   __syncthreads();
   const double total = cum[nb - 1];
@@ -242,7 +246,7 @@ constexpr int kPairMaxHeads = 64;
 
 __global__ void __launch_bounds__(256) k2_pair(const int* __restrict__ kv_cnt, const int* __restrict__ kv_idx,
                                                int Hq, int nb, int group, int q_head0, int* __restrict__ pairs) {
-  extern __shared__ unsigned bm[];  // [m][W] key-block bitmaps, then [m*(m-1)/2] pair differences
+  extern __shared__ unsigned bm[];  // [m][W] key-block bitmaps, [np] pair differences, [np] pair table
   const int qb = blockIdx.x, g = blockIdx.y;
   int lo, hi;
   kv_group_heads(g, Hq, group, q_head0, lo, hi);
@@ -255,9 +259,14 @@ __global__ void __launch_bounds__(256) k2_pair(const int* __restrict__ kv_cnt, c
     base += units_of_group(h2 - l2, nb);
   }
   const int W = (qb >> 5) + 1;
-  unsigned* diff = bm + m * W;
   const int np = m * (m - 1) / 2;
+  unsigned* diff = bm + m * W;
+  unsigned* pij = diff + np;  // pair t -> (i << 8) | j, i < j, row-major over the upper triangle
   for (int i = threadIdx.x; i < m * W; i += blockDim.x) bm[i] = 0u;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const int t0 = i * (2 * m - i - 1) / 2;
+    for (int j = i + 1; j < m; ++j) pij[t0 + j - i - 1] = (unsigned)((i << 8) | j);
+  }
   __syncthreads();
   for (int i = 0; i < m; ++i) {
     const int item = (lo + i) * nb + qb;
@@ -271,12 +280,7 @@ __global__ void __launch_bounds__(256) k2_pair(const int* __restrict__ kv_cnt, c
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   for (int t = warp; t < np; t += nwarps) {
-    int i = 0, r = t;  // t -> (i, j), i < j, row-major over the upper triangle
-    while (r >= m - 1 - i) {
-      r -= m - 1 - i;
-      ++i;
-    }
-    const int j = i + 1 + r;
+    const int i = pij[t] >> 8, j = pij[t] & 255;
     int c = 0;
     for (int w = lane; w < W; w += 32) c += __popc(bm[i * W + w] ^ bm[j * W + w]);
     c = __reduce_add_sync(0xffffffffu, c);
@@ -289,12 +293,7 @@ __global__ void __launch_bounds__(256) k2_pair(const int* __restrict__ kv_cnt, c
     // key = difference (<= nb < 2^20), then i, then j: the smallest key wins
     unsigned best = 0xffffffffu;
     for (int t = lane; t < np; t += 32) {
-      int i = 0, r = t;
-      while (r >= m - 1 - i) {
-        r -= m - 1 - i;
-        ++i;
-      }
-      const int j = i + 1 + r;
+      const int i = pij[t] >> 8, j = pij[t] & 255;
       if (((used >> i) & 1ull) || ((used >> j) & 1ull)) continue;
       best = min(best, (diff[t] << 12) | (unsigned)(i << 6) | (unsigned)j);
     }
@@ -438,7 +437,7 @@ int launch_sched(const int* kv_cnt, const int* kv_idx, int Hq, int nb, int group
       kv_group_heads(g, Hq, group, q_head0, lo, hi);
       m = std::max(m, (hi - lo) & ~1);
     }
-    const size_t psmem = ((size_t)m * ((nb + 31) / 32) + (size_t)m * (m - 1) / 2) * 4;
+    const size_t psmem = ((size_t)m * ((nb + 31) / 32) + (size_t)m * (m - 1)) * 4;
     if (m >= 4 && m <= kPairMaxHeads && psmem <= 200 * 1024) {  // m == 2 has one possible pairing
       set_smem_attr(reinterpret_cast<const void*>(&k2_pair), (int)psmem);
       k2_pair<<<dim3(nb, G), 256, psmem, st>>>(kv_cnt, kv_idx, Hq, nb, group, q_head0, scratch);

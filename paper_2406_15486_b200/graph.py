@@ -12,7 +12,8 @@ result appears in `out`.
 
 The captured work is exactly sample_attention's (stage 1 block_reduce, stage 2
 select + guard + merge + schedule, stage 3 sparse_attention); only the NaN/Inf
-check becomes asynchronous (a device flag read by `check()`).
+check becomes asynchronous (a device flag and the stage-3 status read by
+`check()`).
 """
 
 from __future__ import annotations
@@ -22,7 +23,7 @@ import torch
 from . import _lib
 from .config import plan_chunks, resolve_config
 from .errors import InputError
-from .heads import HeadBatch, check_finite_async, raise_on_flags
+from .heads import HeadBatch, raise_on_flags, scan_inputs_async
 from .stages import block_reduce, merge_index, private_workspace, sample_scores, select, sparse_attention
 
 __all__ = ["SampleAttentionGraph"]
@@ -73,7 +74,7 @@ class SampleAttentionGraph:
     def _stage1(self):
         b = self.batch
         self.flag.zero_()
-        check_finite_async((b.q, b.k, b.v), self.flag, b.stream)
+        self._rescan = b.q if scan_inputs_async(b.q, b.k, b.v, self.flag, b.stream) else None
         return block_reduce(sample_scores(b, self.plan), self.cfg.blk)
 
     def _stage2(self, reduced):
@@ -101,7 +102,7 @@ class SampleAttentionGraph:
     def check(self) -> None:
         """Raise InputError if the last replay saw NaN/Inf in q/k/v, or the
         reference's stage-3 errors from the device status word (host sync)."""
-        raise_on_flags(self.flag, self.batch.q.device)
+        raise_on_flags(self.flag, self.batch.q.device, self._rescan)
 
     def n_rescored(self) -> int:
         return self.selection.n_rescored()

@@ -20,7 +20,7 @@ from . import _lib
 from .errors import InputError, InternalInvariantError
 
 __all__ = ["AttentionHead", "HeadSet", "HeadBatch", "check_finite", "check_finite_async", "check_status", "dcall",
-           "raise_on_flags"]
+           "raise_on_flags", "scan_inputs_async"]
 
 _DTYPES = {torch.bfloat16: _lib.SA_BF16, torch.float32: _lib.SA_FP32}
 
@@ -136,7 +136,11 @@ def check_status(device: torch.device) -> None:
     blocks (ref executor.py:131-132), InternalInvariantError for a mask that
     breaks the BlockMask invariants (filtering.py:97-106) or an empty softmax
     normaliser (executor.py:150-153)."""
-    bits, h, qb, n = _read_status(device)
+    _raise_status(_read_status(device))
+
+
+def _raise_status(status: list) -> None:
+    bits, h, qb, n = status
     if not bits:
         return
     where = f"head {h} query block {qb}" + (f" (and {n - 1} more)" if n > 1 else "")
@@ -148,15 +152,38 @@ def check_status(device: torch.device) -> None:
     raise InternalInvariantError(f"query block {qb} produced an empty softmax normalizer ({where})")
 
 
-def raise_on_flags(finite_flag: torch.Tensor | None, device: torch.device) -> None:
+def scan_inputs_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, flag: torch.Tensor, stream: int) -> bool:
+    """Queue the NaN/Inf scan of the inputs (core.py:30-37).  Returns True when
+    q was left out: on the bf16 path every query row runs through stage 3, and
+    a NaN/Inf anywhere in a row makes that row's softmax normaliser non-finite
+    (every logit of the row is NaN or +-Inf), which the kernel reports in the
+    status word -- so the 1 GB scan of q at 128K is skipped and q is rescanned
+    only when that status bit comes back (raise_on_flags)."""
+    fused = q.dtype == torch.bfloat16
+    check_finite_async((k, v) if fused else (q, k, v), flag, stream)
+    return fused
+
+
+def raise_on_flags(finite_flag: torch.Tensor | None, device: torch.device, rescan_q: torch.Tensor | None = None) -> None:
     """One host sync for everything a call checked on the device: the NaN/Inf
     flag of its inputs (InputError, core.py:30-37) first, then the stage-3
     status word (a non-finite input also poisons the normaliser, so the input
-    error wins and the status is cleared)."""
+    error wins and the status is cleared).  With `rescan_q` (q's scan was left
+    to stage 3, scan_inputs_async) a non-finite normaliser triggers the scan of
+    q, so a NaN/Inf in q still raises InputError."""
     bad_input = finite_flag is not None and int(finite_flag.item()) != 0
     if bad_input:
         _read_status(device)
         raise InputError("q/k/v contain NaN or Inf")
+    if rescan_q is not None:
+        bits = _read_status(device)
+        if bits[0] & _lib.SA_STATUS_NORMALISER:
+            f = torch.zeros(1, dtype=torch.int32, device=rescan_q.device)
+            check_finite_async((rescan_q,), f, _stream(rescan_q))
+            if int(f.item()) != 0:
+                raise InputError("q/k/v contain NaN or Inf")
+        _raise_status(bits)
+        return
     check_status(device)
 
 

@@ -19,7 +19,7 @@ import torch
 
 from .config import ChunkPlan, SparseConfig, n_blocks, plan_chunks, resolve_config
 from .errors import InputError
-from .heads import HeadBatch, HeadSet, check_finite_async, check_status, raise_on_flags
+from .heads import HeadBatch, HeadSet, check_finite_async, check_status, raise_on_flags, scan_inputs_async
 from .masks import BlockMask
 from .stages import (FlopReport, block_reduce, flop_accounting, merge_index, sample_scores, sampled_retained,
                      select, sparse_attention)
@@ -72,9 +72,11 @@ def sample_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, alpha: f
     check_inputs=False leaves the call free of host synchronisation."""
     batch = HeadBatch.from_tensors(q, k, v, group=group, q_head0=q_head0)
     flag = None
+    rescan = None
     if check_inputs:
         flag = torch.zeros(1, dtype=torch.int32, device=batch.q.device)
-        check_finite_async((batch.q, batch.k, batch.v), flag, batch.stream)
+        if scan_inputs_async(batch.q, batch.k, batch.v, flag, batch.stream):
+            rescan = batch.q
     cfg = resolve_config(batch.S, alpha, alpha_c, alpha_s, chunk_n, sample_ratio, blk)
     plan = plan_chunks(batch.S, cfg)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings else None
@@ -93,7 +95,7 @@ def sample_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, alpha: f
     if ev:
         ev[3].record()
     if check_inputs:
-        raise_on_flags(flag, batch.q.device)
+        raise_on_flags(flag, batch.q.device, rescan)
     return o, SampleAttentionResult(cfg, plan, mask, sel.flags, ev, lse)
 
 

@@ -171,7 +171,10 @@ def _run(q, k, v, out, st_, dev, group, hpg, cfg, plan, check_inputs, sink_block
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     compute.wait_event(sampled)
     ev[0].record(compute)
-    if check_inputs:  # the reference's NaN/Inf check (core.py:30-37), read once at the end
+    # the reference's NaN/Inf check (core.py:30-37), read once at the end; q's
+    # own scan is left to stage 3's normaliser check (scan_inputs_async)
+    fused = dq.dtype == torch.bfloat16
+    if check_inputs:
         check_finite_async([dk], flag, compute.cuda_stream)
     batch = HeadBatch.from_tensors(dq, dk, dv, group=group)
     reduced = block_reduce(sample_scores(batch, plan), cfg.blk)
@@ -189,7 +192,8 @@ def _run(q, k, v, out, st_, dev, group, hpg, cfg, plan, check_inputs, sink_block
         if check_inputs:
             if i == 0:
                 check_finite_async([dv], flag, st.cuda_stream)
-            check_finite_async([dq[h0:h1]], flag, st.cuda_stream)
+            if not fused:
+                check_finite_async([dq[h0:h1]], flag, st.cuda_stream)
         kv0, kv1 = h0 // group, (h1 - 1) // group + 1
         with torch.cuda.stream(st):
             part = HeadBatch.from_tensors(dq[h0:h1], dk[kv0:kv1], dv[kv0:kv1], group=group, q_head0=h0)
@@ -208,5 +212,5 @@ def _run(q, k, v, out, st_, dev, group, hpg, cfg, plan, check_inputs, sink_block
     # `out` is host memory: the caller may read it as soon as we return
     d2h.synchronize()
     if check_inputs:
-        raise_on_flags(flag, dev)
+        raise_on_flags(flag, dev, dq if fused else None)
     return out, [SampleAttentionResult(cfg, plan, mask, sel.flags, ev, None)]

@@ -514,3 +514,36 @@ def test_schedule_overlap_pairing(sa, Hq, Hkv, S):
     assert rc == 0
     torch.cuda.synchronize()
     assert torch.equal(out, o2)
+
+
+@pytest.mark.parametrize("where,val", [((0, 0, 0), float("nan")), ((1, 700, 5), float("inf")),
+                                       ((2, 1023, 127), float("-inf")), ((3, 129, 64), float("nan"))])
+def test_nonfinite_q_raises_input_error_on_every_path(sa, where, val):
+    """On the bf16 path q's NaN/Inf scan is left to stage 3 (a non-finite
+    element poisons its row's normaliser; heads.scan_inputs_async), so a single
+    bad element of q -- first row, last row, any dim -- must still raise
+    InputError, through sample_attention, the graph executor and the host path;
+    a bad k or v element is caught by their own scans; and a clean call after a
+    failed one is unaffected."""
+    from paper_2406_15486_b200 import synth
+    q, k, v, _ = synth.make_inputs(1024, 4, 2, 128, seed=11, device="cuda")
+    bad = q.clone()
+    bad[where] = val
+    with pytest.raises(sa.InputError):
+        sa.sample_attention(bad, k, v, alpha=0.95, chunk_n=2)
+    o, _ = sa.sample_attention(q, k, v, alpha=0.95, chunk_n=2)
+    assert torch.isfinite(o.float()).all()
+    g = sa.SampleAttentionGraph(bad, k, v, alpha=0.95, chunk_n=2)
+    g.replay()
+    with pytest.raises(sa.InputError):
+        g.check()
+    with pytest.raises(sa.InputError):
+        sa.sample_attention_host(bad.cpu(), k.cpu(), v.cpu(), alpha=0.95, chunk_n=2)
+    kb = k.clone()
+    kb[1, 1000, 3] = val
+    with pytest.raises(sa.InputError):
+        sa.sample_attention(q, kb, v, alpha=0.95, chunk_n=2)
+    vb = v.clone()
+    vb[0, 5, 100] = val
+    with pytest.raises(sa.InputError):
+        sa.sample_attention(q, k, vb, alpha=0.95, chunk_n=2)
