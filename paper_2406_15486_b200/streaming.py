@@ -43,7 +43,7 @@ def _as_host(x) -> torch.Tensor:
 def _group_plan(Hq: int, group: int, hpg: int) -> list:
     """Stage-3 head groups [h0, h1) inside KV-group boundaries.  A head's Q
     crosses PCIe in ~0.6x the time its stage 3 takes (128K), so the groups
-    ramp up (2, 3, 5 heads, then `hpg`): each group's copy hides under the
+    ramp up (2, 2, 3, 5 heads, then `hpg`): each group's copy hides under the
     previous group's kernels.  The last groups shrink (3, 2, then 1 head):
     each group's output copy hides under the next group's kernels and the
     copy after the last kernel is short."""
@@ -57,7 +57,7 @@ def _group_plan(Hq: int, group: int, hpg: int) -> list:
                     tail.insert(0, s)
                     rest -= s
         if g == 0:
-            for s in (2, 3, 5):
+            for s in (2, 2, 3, 5):
                 if rest > s:
                     head.append(s)
                     rest -= s
@@ -115,6 +115,8 @@ class _Staging:
         self.h2d = torch.cuda.Stream(device=dev)
         self.d2h = torch.cuda.Stream(device=dev)
         self.side = torch.cuda.Stream(device=dev)
+        # stages 1-2 of the later KV groups: high priority, so their CTAs take SMs as stage-3 CTAs retire
+        self.s12 = torch.cuda.Stream(device=dev, priority=-1)
         self.lock = threading.Lock()
 
 
@@ -144,73 +146,114 @@ def _run(q, k, v, out, st_, dev, group, hpg, cfg, plan, check_inputs, sink_block
     Hq, S = q.shape[0], q.shape[1]
     dq, dk, dv, dout = st_.dq, st_.dk, st_.dv, st_.dout
     compute = torch.cuda.current_stream(dev)
-    h2d, d2h, side = st_.h2d, st_.d2h, st_.side
+    h2d, d2h, side, s12 = st_.h2d, st_.d2h, st_.side, st_.s12
     h2d.wait_stream(compute)  # the previous call's readers of dq/dk/dv and this call's inputs
     groups = _group_plan(Hq, group, hpg)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    ready = []
+    fused = dq.dtype == torch.bfloat16  # q's NaN/Inf scan left to stage 3 (scan_inputs_async)
+    # phase 0 = the first KV group, phase 1 = the rest: stage 3 starts after the
+    # first group's K and filtering only, and the other groups' stages 1-2 run on
+    # their own stream while it computes
+    n_kv = Hq // group
+    phases = [(0, 1), (1, n_kv)] if n_kv > 1 else [(0, 1)]
+    row_bytes = q.shape[2] * q.element_size()
+    sampled, ready = [], []
     # the copy stream carries copies only: a kernel queued on it (the NaN/Inf
     # scan) would wait for SMs behind a running stage-3 launch and hold up
     # every copy behind it
-    row_bytes = q.shape[2] * q.element_size()
-    with torch.cuda.stream(h2d):
-        # K (stage 1 reads every key) and the sampled query windows of every head, then V
-        dk.copy_(k, non_blocking=True)
+    def send_filter_inputs(p):  # K (stage 1 reads every key) and the sampled query windows of phase p
+        g0, g1 = phases[p]
+        hs0, hs1 = g0 * group, g1 * group
+        dk[g0:g1].copy_(k[g0:g1], non_blocking=True)
         for c in plan.chunks:
-            off = c.sample_start * row_bytes
+            off = (hs0 * S + c.sample_start) * row_bytes
             dcall(dev, "sa_copy2d_async", dq.data_ptr() + off, S * row_bytes, q.data_ptr() + off, S * row_bytes,
-                  (c.sample_end - c.sample_start) * row_bytes, Hq, h2d.cuda_stream)
-        sampled = torch.cuda.Event()
-        sampled.record(h2d)
-        dv.copy_(v, non_blocking=True)
-        for h0, h1 in groups:  # the rest of Q, group by group (the windows are sent again; same bits)
-            dq[h0:h1].copy_(q[h0:h1], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(h2d)
-            ready.append(ev)
+                  (c.sample_end - c.sample_start) * row_bytes, hs1 - hs0, h2d.cuda_stream)
+        e = torch.cuda.Event()
+        e.record(h2d)
+        sampled.append(e)
+
+    # order: phase 0's K + windows + V, its first Q group, then the other
+    # phases' K + windows (their filtering then overlaps the first stage-3
+    # launches instead of waiting behind them for SMs), the rest of Q and V
+    with torch.cuda.stream(h2d):
+        send_filter_inputs(0)
+        dv[0:1].copy_(v[0:1], non_blocking=True)
+        first_v = {0}
+        for i, (h0, h1) in enumerate(groups):
+            g = h0 // group
+            p = 0 if g < phases[0][1] else 1
+            if p == 1 and len(sampled) == 1:  # no first-phase group followed (single head group)
+                send_filter_inputs(1)
+            if g not in first_v:
+                gp0, gp1 = phases[p]
+                dv[gp0:gp1].copy_(v[gp0:gp1], non_blocking=True)
+                first_v.update(range(gp0, gp1))
+            dq[h0:h1].copy_(q[h0:h1], non_blocking=True)  # the windows are sent again; same bits
+            e = torch.cuda.Event()
+            e.record(h2d)
+            ready.append(e)
+            if i == 0 and len(phases) > 1:
+                send_filter_inputs(1)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    compute.wait_event(sampled)
-    ev[0].record(compute)
-    # the reference's NaN/Inf check (core.py:30-37), read once at the end; q's
-    # own scan is left to stage 3's normaliser check (scan_inputs_async)
-    fused = dq.dtype == torch.bfloat16
-    if check_inputs:
-        check_finite_async([dk], flag, compute.cuda_stream)
-    batch = HeadBatch.from_tensors(dq, dk, dv, group=group)
-    reduced = block_reduce(sample_scores(batch, plan), cfg.blk)
-    ev[1].record(compute)
-    sel = select(reduced, cfg, guard=guard)
-    mask = merge_index(sel, plan, cfg.blk, S, sink_blocks, local_blocks)
-    ev[2].record(compute)
+    lanes = (compute, side, s12)
+    side.wait_stream(compute)
+    s12.wait_stream(compute)
+    masks, results = [], []
+    for p, (g0, g1) in enumerate(phases):  # stages 1-2 per phase
+        st = compute if p == 0 else s12
+        st.wait_event(sampled[p])
+        if p == 0:
+            ev[0].record(st)
+        hs0, hs1 = g0 * group, g1 * group
+        with torch.cuda.stream(st):
+            if check_inputs:  # the reference's NaN/Inf check (core.py:30-37), read once at the end
+                check_finite_async([dk[g0:g1]], flag, st.cuda_stream)
+            batch = HeadBatch.from_tensors(dq[hs0:hs1], dk[g0:g1], dv[g0:g1], group=group, q_head0=hs0)
+            reduced = block_reduce(sample_scores(batch, plan), cfg.blk)
+            if p == 0:
+                ev[1].record(st)
+            sel = select(reduced, cfg, guard=guard)
+            mask = merge_index(sel, plan, cfg.blk, S, sink_blocks, local_blocks)
+            if p == 0:
+                ev[2].record(st)
+        done_p = torch.cuda.Event()
+        done_p.record(st)
+        masks.append((hs0, hs1, mask, done_p))
+        results.append(SampleAttentionResult(cfg, plan, mask, sel.flags, ev if p == 0 else None, None))
     # stage-3 launches alternate between two streams, so a group's kernel fills
     # the SMs the previous group's last wave leaves idle
-    side.wait_stream(compute)
-    lanes = (compute, side)
     for i, ((h0, h1), landed) in enumerate(zip(groups, ready)):
         st = lanes[i % _lanes]
         st.wait_event(landed)
+        hs0, hs1, mask, done_p = next(m for m in masks if m[0] <= h0 < m[1])
+        st.wait_event(done_p)
+        kv0, kv1 = h0 // group, (h1 - 1) // group + 1
         if check_inputs:
-            if i == 0:
-                check_finite_async([dv], flag, st.cuda_stream)
+            if h0 == hs0:
+                check_finite_async([dv[kv0:kv1]], flag, st.cuda_stream)
             if not fused:
                 check_finite_async([dq[h0:h1]], flag, st.cuda_stream)
-        kv0, kv1 = h0 // group, (h1 - 1) // group + 1
         with torch.cuda.stream(st):
             part = HeadBatch.from_tensors(dq[h0:h1], dk[kv0:kv1], dv[kv0:kv1], group=group, q_head0=h0)
-            sparse_attention(part, mask.heads(h0, h1), out=dout[h0:h1], report=False)
+            sparse_attention(part, mask.heads(h0 - hs0, h1 - hs0), out=dout[h0:h1], report=False)
         done = torch.cuda.Event()
         done.record(st)
         d2h.wait_event(done)
         with torch.cuda.stream(d2h):
             out[h0:h1].copy_(dout[h0:h1], non_blocking=True)
     compute.wait_stream(side)
+    compute.wait_stream(s12)
     ev[3].record(compute)
     compute.wait_stream(d2h)
     flag.record_stream(side)
-    for t in (mask.kv_cnt, mask.kv_idx):
-        t.record_stream(side)
+    flag.record_stream(s12)
+    for _, _, m, _ in masks:
+        for t in (m.kv_cnt, m.kv_idx):
+            t.record_stream(side)
+            t.record_stream(compute)
     # `out` is host memory: the caller may read it as soon as we return
     d2h.synchronize()
     if check_inputs:
         raise_on_flags(flag, dev, dq if fused else None)
-    return out, [SampleAttentionResult(cfg, plan, mask, sel.flags, ev, None)]
+    return out, results
