@@ -19,7 +19,9 @@ from .pipeline import (ORACLE_CAP, HeadMetrics, MetricsReport, SampleAttentionRe
                        run_pipeline, sample_attention)
 from . import tensor_io
 from .graph import SampleAttentionGraph
-from .streaming import sample_attention_host
+from . import refsynth, streaming
+from .refsynth import SyntheticSpec, generate_synthetic
+from .streaming import release_staging, sample_attention_host
 from .stages import (GUARD_EPS, ChunkScores, FlopReport, ReducedScores, SampledScores, arg_topk, block_reduce,
                      find_k, flop_accounting, merge_index, sample_scores, select, select_and_merge,
                      sparse_attention)
@@ -32,6 +34,6 @@ __all__ = [
     "InternalInvariantError", "MetricsReport", "SampleAttentionGraph", "ORACLE_CAP", "ReducedScores", "SampleAttentionResult",
     "SampledRange", "SampledScores", "SelectedIndices", "SparseConfig", "arg_topk", "block_reduce",
     "check_finite", "cra_full", "dense_attention", "find_k", "flop_accounting", "merge_index", "n_blocks", "plan_chunks",
-    "resolve_config", "run_pipeline", "sample_attention", "sample_attention_host", "sample_scores", "select", "select_and_merge",
-    "sparse_attention",
+    "release_staging", "resolve_config", "run_pipeline", "sample_attention", "sample_attention_host", "sample_scores",
+    "select", "select_and_merge", "sparse_attention", "SyntheticSpec", "generate_synthetic",
 ]
