@@ -157,11 +157,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       // every key of the block is causal for every row of the window: no per-element mask (warp-uniform)
       const bool full = kb * 128 + 127 < ss;
       float mx = -INFINITY;
+      uint32_t rb[2][32];  // TMEM loads double-buffered: chunk ch+1 in flight while ch is reduced
+      tmem_ld32(taddr, rb[0]);
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
-        uint32_t r[32];
-        tmem_ld32(taddr + ch * 32, r);
-        tmem_ld_wait();
+        uint32_t(&r)[32] = rb[ch & 1];
+        tmem_ld_wait_regs(r);
+        if (ch < 3) tmem_ld32(taddr + (ch + 1) * 32, rb[(ch + 1) & 1]);
         if (full) {
           float mb = -INFINITY;
 #pragma unroll
@@ -179,33 +181,37 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
       const float m_new = fmaxf(m_run, mx * sl2);
-      float a = 0.f, b = 0.f;
+      // four independent add chains per sum (t & 3), so the adds do not serialise on their latency
+      float ac[4] = {0.f, 0.f, 0.f, 0.f}, bc[4] = {0.f, 0.f, 0.f, 0.f};
       // warp-collective TMEM loads stay outside any per-row condition
       const int lim_e = m_new == -INFINITY ? -1 : lim;
+      tmem_ld32(taddr, rb[0]);
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
-        uint32_t r[32];
-        tmem_ld32(taddr + ch * 32, r);
-        tmem_ld_wait();
-        if (full) {  // same values (FFMA2 = two fused FMAs) and summation order as the masked loop
+        uint32_t(&r)[32] = rb[ch & 1];
+        tmem_ld_wait_regs(r);
+        if (ch < 3) tmem_ld32(taddr + (ch + 1) * 32, rb[(ch + 1) & 1]);
+        if (full) {  // same values (FFMA2 = two fused FMAs) as the masked loop
           const uint64_t negm = f32x2(-m_new, -m_new), sl2x2 = f32x2(sl2, sl2);
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
             float y0, y1;
             unpack_f32x2(ffma2(f32x2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, negm), y0, y1);
             const float p0 = ex2(y0), p1 = ex2(y1);
-            if (ch * 32 + i <= rho) a += p0; else b += p0;
-            if (ch * 32 + i + 1 <= rho) a += p1; else b += p1;
+            if (ch * 32 + i <= rho) ac[i & 3] += p0; else bc[i & 3] += p0;
+            if (ch * 32 + i + 1 <= rho) ac[(i + 1) & 3] += p1; else bc[(i + 1) & 3] += p1;
           }
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int t = ch * 32 + i;
             const float p = t <= lim_e ? ex2(fmaf(__uint_as_float(r[i]), sl2, -m_new)) : 0.f;
-            if (t <= rho) a += p; else b += p;
+            if (t <= rho) ac[i & 3] += p; else bc[i & 3] += p;
           }
         }
       }
+      const float a = (ac[0] + ac[1]) + (ac[2] + ac[3]);
+      const float b = (bc[0] + bc[1]) + (bc[2] + bc[3]);
       tc_fence_before();
       mbar_arrive(&sm->s_empty[buf]);
       if (valid) {

@@ -38,16 +38,17 @@ __all__ = [
     "sparse_attention", "flop_accounting", "as_batch", "sampled_retained",
 ]
 
-# 5x the worst prefix-sum error of the tensor-core scores measured at 96K-128K
-# (tools/guard_diag.py: max |cum_tc - cum_exact| / total = 7.9e-8)
+# ~7x the worst prefix-sum error of the tensor-core scores measured at 96K-128K
+# (tools/guard_diag.py, profiles/r2/guard_*.txt: max |cum_tc - cum_exact| / total
+# = 5.5e-8 at C3, 1.0e-7 at C4 with 10 % sampling)
 GUARD_EPS = 4e-7
 # The tensor-core error grows with sum_i |q_i k_i|, bounded per (head, chunk)
 # by B = max ||q_r|| * max ||k_j|| / sqrt(d) (sa_stage1's logit bound).
-# Measured (profiles/r2c: C3, C4 at 10 % sampling, and large-logit / heavy-sink
-# heads up to B = 930): prefix-sum error / total <= 4.7e-10 * B.  GUARD_EPS
-# applies up to B = GUARD_LOGIT_REF (the synthetic benchmark heads reach 305);
-# above it the margin grows in proportion, keeping it >= 2.7x the worst
-# measured error at every B.
+# Measured (C3, C4 at 10 % sampling, and large-logit / heavy-sink heads up to
+# B = 930): prefix-sum error / total <= 4.75e-10 * B.  GUARD_EPS applies up to
+# B = GUARD_LOGIT_REF (the synthetic benchmark heads reach 305); above it the
+# margin grows in proportion, keeping it >= 2.6x the worst measured error at
+# every B.
 GUARD_LOGIT_REF = 320.0
 
 _WS_CACHE: dict = {}

@@ -20,7 +20,7 @@ from paper_2406_15486_b200.errors import GeneratorError, InputError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 FX = json.load(open(os.path.join(HERE, "golden", "refsynth.json")))
-DEV = "cuda" if torch.cuda.is_available() else "cpu"
+DEV = "cpu"  # the CPU suite; test_generator_on_the_gpu repeats the check on the device path
 
 
 def _spec(kw):
@@ -80,3 +80,20 @@ def test_gqa_inputs_share_planted_dims():
                                     refsynth._control_offsets(spec))
     got = np.concatenate([sm, bm])
     assert np.all(np.abs(got / spec.targets() - 1.0) <= 0.2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", FX["specs"][:2], ids=lambda c: f"S{c['spec']['S']}")
+def test_generator_on_the_gpu(case):
+    """The same reference comparison with the mass measurements on the GPU
+    (fp64 matmuls / exp / cumsum on the device)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    spec = _spec(case["spec"])
+    heads = refsynth.generate_synthetic(spec, device="cuda")
+    for h, want in zip(heads, case["heads"]):
+        rows = np.array(want["rows"])
+        np.testing.assert_allclose(h.q.cpu().numpy()[rows], np.array(want["q_rows"]), rtol=1e-9, atol=1e-9)
+        np.testing.assert_allclose(h.k.cpu().numpy()[rows], np.array(want["k_rows"]), rtol=1e-9, atol=1e-9)
+        np.testing.assert_allclose(h.sink_mass, want["sink_mass"], rtol=1e-9)
+        np.testing.assert_allclose(h.band_mass, want["band_mass"], rtol=1e-9, atol=1e-12)

@@ -1,7 +1,8 @@
-"""Exact (fp64, DMMA) stage-1 pass over every (head, chunk) pair, timed per
-library build (interleaved), plus the max |col - col(first build)|.
+"""Stage-1 pass over every (head, chunk) pair -- exact (fp64, DMMA) or tensor
+(tcgen05) mode -- timed per library build (interleaved), plus the max
+relative |col - col(first build)|.
 
-    python tools/exact_bench.py --libs a.so b.so [--config c2] [--reps 5]
+    python tools/exact_bench.py --libs a.so b.so [--config c2] [--chunk-n 77] [--mode tensor] [--reps 5]
 """
 import argparse
 import ctypes
@@ -18,6 +19,8 @@ def main():
     ap.add_argument("--libs", nargs="+")
     ap.add_argument("--config", default="c2")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--mode", choices=["exact", "tensor"], default="exact")
+    ap.add_argument("--chunk-n", type=int, default=None)
     a = ap.parse_args()
     import torch
     import bench
@@ -27,7 +30,8 @@ def main():
     S, Hq, Hkv, alpha, cn, _ = bench.CONFIGS[a.config]
     q, k, v, _ = synth.make_inputs(S, Hq, Hkv, 128, seed=0, device="cuda")
     b = sa.HeadBatch.from_tensors(q, k, v)
-    plan = sa.plan_chunks(S, sa.SparseConfig(chunk_n=cn))
+    plan = sa.plan_chunks(S, sa.SparseConfig(chunk_n=a.chunk_n or cn))
+    mode = _lib.SA_STAGE1_EXACT if a.mode == "exact" else _lib.SA_STAGE1_TENSOR
     nb = -(-S // 128)
     ws = _workspace(b, 128, plan.chunk_n)
     st = torch.cuda.current_stream().cuda_stream
@@ -42,7 +46,7 @@ def main():
 
     def run(i):
         rc = libs[i][1](q.data_ptr(), k.data_ptr(), _lib.SA_BF16, S, Hq, Hkv, 128, 128, b.group, 0, plan.chunk_n,
-                        plan.itv, cols[i].data_ptr(), slash.data_ptr(), None, _lib.SA_STAGE1_EXACT, None,
+                        plan.itv, cols[i].data_ptr(), slash.data_ptr(), None, mode, None,
                         ws.data_ptr(), ws.numel(), st)
         assert rc == 0, rc
 
