@@ -29,10 +29,13 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kRows = 128;
 constexpr int kKeys = 128;
-constexpr int kDChunk = 32;      // head-dim slice of K staged per round (double-buffered)
-constexpr int kPitchQ = 132;     // fp64 smem pitches = 4 (mod 32): conflict-free m8n8k4 fragment loads
-constexpr int kPitchK = 36;
-constexpr int kXfSmemBytes = (kRows * kPitchQ + 2 * kKeys * kPitchK) * 8;
+constexpr int kDChunk = 64;      // head-dim slice of K staged per round (double-buffered, fp64)
+constexpr int kPitchQ = 132;     // smem pitches: conflict-free m8n8k4 fragment loads (Q raw, K fp64 = 4 mod 32)
+constexpr int kPitchK = 68;
+template <typename T>
+constexpr int xf_smem_bytes() {  // Q raw (T), then two fp64 K slices (8-byte aligned: kRows * kPitchQ * 2 % 8 == 0)
+  return kRows * kPitchQ * (int)sizeof(T) + 2 * kKeys * kPitchK * 8;
+}
 
 struct Win {
   int ss, se, nkb;  // sampled rows [ss, se); key blocks 0..nkb-1 hold keys < se
@@ -58,40 +61,32 @@ __device__ __forceinline__ float to_f<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-// 8 consecutive elements of row r, dims [c, c+8), of a row-major [n, d]
-// matrix (zero past n rows / d dims); one 16-byte load per 8 bf16 (or two per
-// 8 floats) when d allows it.
+// 16 consecutive elements of row r, dims [c, c+16), of a row-major [n, d]
+// matrix, zero past n rows / d dims, held RAW (8 registers for bf16): 16-byte
+// loads when d allows it; converted to fp64 only when stored into the smem slice.
 template <typename T>
-struct Oct {
-  double v[8];
+struct Slice16 {
+  T v[16];
   __device__ __forceinline__ void load(const T* __restrict__ src, int r, int n, int c, int d) {
     if (r >= n || c >= d) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = 0.0;
+      for (int i = 0; i < 16; ++i) v[i] = T(0.f);
       return;
     }
     const T* p = src + (size_t)r * d + c;
-    if (c + 8 <= d && d % 8 == 0) {
-      if constexpr (sizeof(T) == 2) {
-        const uint4 u = *reinterpret_cast<const uint4*>(p);
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    if (c + 16 <= d && d % 8 == 0) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          v[2 * i] = (double)__uint_as_float(w[i] << 16);
-          v[2 * i + 1] = (double)__uint_as_float(w[i] & 0xffff0000u);
-        }
-      } else {
-        const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
-        v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
-      }
+      for (int i = 0; i < (int)(16 * sizeof(T) / 16); ++i)
+        reinterpret_cast<uint4*>(v)[i] = reinterpret_cast<const uint4*>(p)[i];
       return;
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = c + i < d ? (double)to_f(p[i]) : 0.0;
+    for (int i = 0; i < 16; ++i) v[i] = c + i < d ? p[i] : T(0.f);
   }
   __device__ __forceinline__ void store(double* dst) const {
 #pragma unroll
-    for (int i = 0; i < 8; i += 2) *reinterpret_cast<double2*>(dst + i) = make_double2(v[i], v[i + 1]);
+    for (int i = 0; i < 16; i += 2)
+      *reinterpret_cast<double2*>(dst + i) = make_double2((double)to_f(v[i]), (double)to_f(v[i + 1]));
   }
 };
 
@@ -102,14 +97,15 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 }
 
 // Work of one CTA: key blocks [kb0, kb1) of (head, chunk) hc.  The window's
-// query rows are staged once (fp64, all d dims); K streams through two
-// 32-dim smem buffers, the next slice's global loads issued into registers
-// before the current slice's MMAs so their latency hides under them.  Lane
-// (gq = lane / 4, tg = lane % 4) of warp w holds rows 8w + gq, keys 8nt + 2tg + {0, 1}.
+// query rows are staged once, raw (converted to fp64 per MMA fragment: one
+// conversion per 16 MMAs); K streams through two 64-dim fp64 smem slices, the
+// next slice's global loads issued into registers before the current slice's
+// MMAs so their latency hides under them.  Lane (gq = lane / 4, tg = lane % 4)
+// of warp w holds rows 8w + gq, keys 8nt + 2tg + {0, 1}.
 template <typename T>
 __device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __restrict__ k, const Stage1Geom& g,
                                         int hc, int kb0, int kb1, double* __restrict__ pa,
-                                        double* __restrict__ pb, double* __restrict__ pm, double* qs,
+                                        double* __restrict__ pb, double* __restrict__ pm, T* qs,
                                         double* ks) {
   const int h = hc / g.cn, c = hc - h * g.cn;
   const Win w = window_of(c, g.S, g.blk, g.itv);
@@ -122,17 +118,14 @@ __device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __rest
   const T* kh = k + (size_t)kvh * g.S * d;
   const double scale = 1.0 / sqrt((double)d);
   const int nch = (d + kDChunk - 1) / kDChunk;  // K slices per key block
-  // staging map: thread -> (row, 8 dims) of a 128 x 32 slice
-  const int sr = threadIdx.x >> 2, sc = (threadIdx.x & 3) * 8;
-  for (int e = threadIdx.x; e < kRows * (kPitchQ / 8); e += kThreads) {  // Q once, all dims
-    const int r = e / (kPitchQ / 8), c8 = (e - r * (kPitchQ / 8)) * 8;
-    if (c8 + 8 > kPitchQ) continue;
-    Oct<T> o;
-    o.load(qh, r, nr, c8, d);
-    o.store(qs + r * kPitchQ + c8);
+  for (int e = threadIdx.x; e < kRows * kPitchQ; e += kThreads) {  // Q once, all dims (zero pad)
+    const int r = e / kPitchQ, cc = e - r * kPitchQ;
+    qs[e] = (r < nr && cc < d) ? qh[(size_t)r * d + cc] : T(0.f);
   }
+  // staging map: thread -> (row, 16 dims) of a 128 x 64 slice
+  const int sr = threadIdx.x >> 2, sc = (threadIdx.x & 3) * 16;
   auto nk_of = [&](int kb) { return min(blk, w.se - kb * blk); };  // keys any sampled row can see
-  Oct<T> nxt;
+  Slice16<T> nxt;
   nxt.load(kh + (size_t)kb0 * blk * d, sr, nk_of(kb0), sc, d);
   nxt.store(ks + sr * kPitchK + sc);
   __syncthreads();
@@ -145,17 +138,17 @@ __device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __rest
 #pragma unroll
     for (int nt = 0; nt < 16; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
     for (int ch = 0; ch < nch; ++ch) {
-      // prefetch the next slice (this block's next 32 dims, or the next block's first)
+      // prefetch the next slice (this block's next 64 dims, or the next block's first)
       const bool more = ch + 1 < nch || kb + 1 < kb1;
       if (more) {
         const int kbn = ch + 1 < nch ? kb : kb + 1, chn = ch + 1 < nch ? ch + 1 : 0;
         nxt.load(kh + (size_t)kbn * blk * d, sr, nk_of(kbn), chn * kDChunk + sc, d);
       }
       const double* kq = ks + buf * (kKeys * kPitchK);
-      const double* qq = qs + (8 * warp + gq) * kPitchQ + ch * kDChunk + tg;
-#pragma unroll
+      const T* qq = qs + (8 * warp + gq) * kPitchQ + ch * kDChunk + tg;
+#pragma unroll 4
       for (int kc = 0; kc < kDChunk; kc += 4) {
-        const double a = qq[kc];
+        const double a = (double)to_f(qq[kc]);
         double b[16];
 #pragma unroll
         for (int nt = 0; nt < 16; ++nt) b[nt] = kq[(8 * nt + gq) * kPitchK + kc + tg];
@@ -216,8 +209,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     xf_pass(const T* __restrict__ q, const T* __restrict__ k, Stage1Geom g, const int* __restrict__ list,
             int kb_per_cta, double* __restrict__ pa, double* __restrict__ pb, double* __restrict__ pm) {
   extern __shared__ double smem_d[];
-  double* qs = smem_d;                    // [kRows][kPitchQ]
-  double* ks = smem_d + kRows * kPitchQ;  // 2 x [kKeys][kPitchK]
+  T* qs = reinterpret_cast<T*>(smem_d);                                                  // [kRows][kPitchQ] raw
+  double* ks = reinterpret_cast<double*>(reinterpret_cast<char*>(smem_d) + kRows * kPitchQ * sizeof(T));  // 2 x slice
   const int n_pairs = list ? list[0] : g.Hq * g.cn;
   const int kb0 = blockIdx.x * kb_per_cta;
   for (int f = blockIdx.y; f < n_pairs; f += gridDim.y) {  // uniform per CTA
@@ -465,7 +458,7 @@ namespace {
 template <typename T>
 int run_exact(const Stage1Geom& g, const T* q, const T* k, const int* only, char* ws, const Workspace& L,
               double* col, double* slash, cudaStream_t st) {
-  const size_t smem = kXfSmemBytes;
+  const size_t smem = xf_smem_bytes<T>();
   set_smem_attr(reinterpret_cast<const void*>(&xf_pass<T>), (int)smem);
   const size_t plane = (size_t)g.Hq * g.cn * g.blk * g.nb;
   double* pa = reinterpret_cast<double*>(ws + L.x_part);

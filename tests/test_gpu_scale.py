@@ -169,3 +169,29 @@ def test_selection_matches_oracle_at_1m(sa):
         for ob in i_s:
             want |= {kb for kb in (qb - ob - 1, qb - ob) if 0 <= kb <= qb}
         assert tuple(int(x) for x in res.mask.head(0).active_for(qb)) == tuple(sorted(want)), qb
+
+
+@pytest.mark.parametrize("config", ["c3", "c4_77"])
+def test_guard_auto_equals_all_fp64_on_every_head(sa, config):
+    """Certifies the selection guard on the full benchmark workloads: with
+    guard="auto" (tensor-core scores, fp64 re-score of the flagged pairs only)
+    every head's selected index sets and merged mask equal those of
+    guard="always" (every pair scored in fp64, the reference's arithmetic) --
+    C3 at alpha 0.90 / 0.95 / 0.98 (32 heads) and C4 at 10 % sampling
+    (32 heads x 77 chunks).  A decision the tensor-core error could flip that
+    the margin test missed would show up here."""
+    import torch
+
+    from paper_2406_15486_b200 import synth
+    if config == "c3":
+        S, Hq, Hkv, cn, alphas = 131072, 32, 2, 1, (0.90, 0.95, 0.98)
+    else:
+        S, Hq, Hkv, cn, alphas = 98304, 32, 8, 77, (0.95,)
+    q, k, v, _ = synth.make_inputs(S, Hq, Hkv, seed=0, device="cuda")
+    for alpha in alphas:
+        _, ra = sa.sample_attention(q, k, v, alpha=alpha, chunk_n=cn, guard="auto")
+        _, rw = sa.sample_attention(q, k, v, alpha=alpha, chunk_n=cn, guard="always")
+        assert ra.n_rescored() < Hq * cn  # the guard re-scored a subset, not everything
+        assert ra.mask.selections() == rw.mask.selections(), alpha
+        assert torch.equal(ra.mask.kv_cnt, rw.mask.kv_cnt), alpha
+        assert np.array_equal(ra.mask.to_dense(), rw.mask.to_dense()), alpha
