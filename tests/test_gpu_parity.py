@@ -547,3 +547,19 @@ def test_nonfinite_q_raises_input_error_on_every_path(sa, where, val):
     vb[0, 5, 100] = val
     with pytest.raises(sa.InputError):
         sa.sample_attention(q, k, vb, alpha=0.95, chunk_n=2)
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,cn,hpg", [(1000, 3, 1, 2, 2), (777, 6, 2, 3, 1), (4096, 4, 4, 2, 8),
+                                            (2048, 16, 2, 1, 3)])
+def test_host_path_shapes(sa, S, Hq, Hkv, cn, hpg):
+    """sample_attention_host over ragged S, MQA, MHA and odd group splits (one
+    or two filtering phases, ramped head groups, pageable inputs) gives the
+    device path's output and masks bit for bit."""
+    from paper_2406_15486_b200 import synth
+    q, k, v, _ = synth.make_inputs(S, Hq, Hkv, 128, seed=S + Hq, device="cuda")
+    o_dev, r_dev = sa.sample_attention(q, k, v, alpha=0.95, chunk_n=cn)
+    o_host, res = sa.sample_attention_host(q.cpu(), k.cpu(), v.cpu(), alpha=0.95, chunk_n=cn, heads_per_group=hpg)
+    assert torch.equal(o_host, o_dev.cpu())
+    grid = np.concatenate([r.mask.to_dense() for r in res])
+    assert np.array_equal(grid, r_dev.mask.to_dense())
+    sa.release_staging()
