@@ -108,18 +108,38 @@ int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, i
 
 /* Stage 2a — replaces find_k + arg_topk per (head, chunk, direction)
  * (filtering.py:30-62, applied as in select_and_merge :245-255).
- * margin_eps > 0 enables the selection guard: flags[h*cn + c] is set to 1
- * when the alpha cut or the boundary tie gap lies within margin_eps * total
- * of a decision, i.e. when scores carrying that relative error could change
- * the reference's answer; with logit_bound (sa_stage1's) the margin of pair
- * hc is margin_eps * max(1, logit_bound[hc] / bound_ref) * total.  With
- * only_flags != NULL only flagged pairs are
- * recomputed.  k_in != NULL ([Hq][cn][2]) skips find_k and takes the given k
- * (the reference's arg_topk(scores, k), filtering.py:51-62). */
+ * margin_eps > 0 (with k_in == NULL) enables the selection guard.  E =
+ * margin_eps * max(1, logit_bound[hc] / bound_ref) * total is the error the
+ * scores of pair hc may carry (logit_bound from sa_stage1, may be NULL):
+ *   - alpha cut within E of a decision (either side): flags[hc] = 1 (the
+ *     pair needs its exact re-score);
+ *   - only the boundary tie within E: the run of blocks around the cut whose
+ *     consecutive gaps are below 2E is recorded in band (sa_band_table_len
+ *     ints: per (hc, dir) [count, first rank, block / bin indices]) for
+ *     sa_refine_bands -- or flags[hc] = 1 when band is NULL, the run is longer
+ *     than 16 blocks, or the cut margins do not cover swaps inside it.
+ * margin_eps > 0 WITH k_in certifies refined scores: flags[hc] = 1 when the
+ * two blocks at the cut differ by less than margin_eps * (scale) * (s_a + s_b).
+ * only_flags != NULL recomputes the flagged pairs only.  k_in != NULL
+ * ([Hq][cn][2]) skips find_k and takes the given k (the reference's
+ * arg_topk(scores, k), filtering.py:51-62). */
 int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int nb,
               double alpha_c, double alpha_s, double margin_eps, const double* logit_bound,
               double bound_ref, int* flags, const int* only_flags, const int* k_in, int* k_out,
-              int* idx_out, void* stream);
+              int* idx_out, int* band, void* stream);
+
+/* Selection guard, band refinement (no reference counterpart: it reproduces the
+ * reference's fp64 ordering of the few nearly tied blocks at a cut).  For each
+ * band recorded by sa_select whose pair is not flagged, the exact (fp64) mass
+ * of every band block / bin over the pair's sampled rows is computed on the
+ * FP64 tensor cores and normalised with stage 1's tensor-core row statistics
+ * (left in the workspace by sa_stage1), and written over that block's col /
+ * slash score; band_pairs[hc] = 1 marks the refined pairs (for the certifying
+ * sa_select).  bf16 path only. */
+int sa_band_table_len(int Hq, int chunk_n);
+int sa_refine_bands(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, int d, int blk, int group,
+                    int q_head0, int chunk_n, int itv, const int* band, const int* flags, int* band_pairs,
+                    double* col, double* slash, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Stage 2b — replaces merge_index (filtering.py:198-230): extends every
  * chunk's picks over its query region, unions straddling blocks, forces the

@@ -23,7 +23,7 @@ namespace sa {
 
 int launch_select(const double* col, const double* slash, int Hq, int cn, int nb, double ac,
                   double as, double eps, const double* bound, double bound_ref, int* flags, const int* only,
-                  const int* k_in, int* k_out, int* idx_out, cudaStream_t st);
+                  const int* k_in, int* k_out, int* idx_out, int* band, cudaStream_t st);
 int launch_merge(const int* k_sel, const int* idx_sel, int Hq, int cn, int nb, int S, int blk,
                  int itv, int sink_blocks, int local_blocks, int* kv_cnt, int* kv_idx,
                  long long* ab, long long* ae, cudaStream_t st);
@@ -131,6 +131,8 @@ Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int d
   off = align_up(off + (size_t)(Hq * cn + 2) * sizeof(int));
   L.kmax2 = off;
   off = align_up(off + (size_t)Hkv * sizeof(unsigned));
+  L.band_items = off;
+  off = align_up(off + (1 + 2 * (size_t)Hq * cn * 2 * kBandItemsPerEntry) * sizeof(int));
   L.total = off;
   return L;
 }
@@ -229,7 +231,7 @@ int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, i
 
 int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int nb, double alpha_c,
               double alpha_s, double margin_eps, const double* logit_bound, double bound_ref, int* flags,
-              const int* only_flags, const int* k_in, int* k_out, int* idx_out, void* stream) {
+              const int* only_flags, const int* k_in, int* k_out, int* idx_out, int* band, void* stream) {
   if (!(alpha_c >= 0.0 && alpha_c <= 1.0))
     return fail(SA_ERR_INVALID, "alpha_c must be in [0, 1]");
   if (!(alpha_s >= 0.0 && alpha_s <= 1.0))
@@ -239,8 +241,26 @@ int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int n
   if (margin_eps > 0.0 && !flags) return fail(SA_ERR_INVALID, "sa_select: guard needs flags");
   if (logit_bound && !(bound_ref > 0.0)) return fail(SA_ERR_INVALID, "sa_select: bound_ref must be > 0");
   return launch_select(col, slash, Hq, chunk_n, nb, alpha_c, alpha_s, margin_eps, logit_bound, bound_ref, flags,
-                       only_flags,
-                       k_in, k_out, idx_out, static_cast<cudaStream_t>(stream));
+                       only_flags, k_in, k_out, idx_out, band, static_cast<cudaStream_t>(stream));
+}
+
+int sa_band_table_len(int Hq, int chunk_n) {
+  if (Hq < 1 || chunk_n < 1) return fail(SA_ERR_INVALID, "sa_band_table_len: bad args");
+  return Hq * chunk_n * 2 * kBandEntry;
+}
+
+int sa_refine_bands(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, int d, int blk, int group,
+                    int q_head0, int chunk_n, int itv, const int* band, const int* flags, int* band_pairs,
+                    double* col, double* slash, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int e = check_geom(S, Hq, Hkv, d, blk, group, q_head0, dtype)) return e;
+  if (!q || !k || !band || !flags || !band_pairs || !col || !slash || !workspace)
+    return fail(SA_ERR_INVALID, "sa_refine_bands: null pointer");
+  const Workspace L = workspace_layout(S, Hq, Hkv, d, blk, chunk_n, dtype);
+  if (workspace_bytes < L.total) return fail(SA_ERR_INVALID, "sa_refine_bands: workspace too small");
+  if (dtype != SA_BF16) return fail(SA_ERR_UNSUPPORTED, "sa_refine_bands: the band guard serves the bf16 path");
+  Stage1Geom g{S, Hq, Hkv, d, blk, group, q_head0, chunk_n, itv, ceil_div(S, blk)};
+  return launch_refine_bands(g, q, k, dtype, band, flags, band_pairs, static_cast<char*>(workspace), L, col, slash,
+                             static_cast<cudaStream_t>(stream));
 }
 
 int sa_merge(const int* k_sel, const int* idx_sel, int Hq, int chunk_n, int nb, int S, int blk,

@@ -54,9 +54,19 @@ struct Workspace {
   size_t part3;     // double [Hq*cn*nb][4]       (col, slash X-1, X, X+1) per key block
   size_t flag_list; // int    [Hq*cn + 2]             compacted guard-flagged pairs: count, then indices
   size_t kmax2;     // uint   [Hkv]                 max ||k_j||^2 per KV head (guard logit bound)
+  size_t band_items;// int    [1 + 2 * n_items]       band refinement work list: count, then (pair, key block)
   size_t total;
 };
 Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int dtype);
+
+// Selection guard, band refinement: per (head, chunk, direction) the run of
+// nearly tied blocks at the cut -- [count, first rank, block / bin indices].
+constexpr int kBandMax = 16;
+constexpr int kBandEntry = 2 + kBandMax;
+
+// key blocks one band entry can need: a slash bin reads two key blocks for each
+// of the (at most two) query blocks a sampled window spans
+constexpr int kBandItemsPerEntry = 4 * kBandMax;
 
 // Launchers (return SA_OK or an error code; all stream-ordered).
 int launch_stage1_exact(const Stage1Geom& g, const void* q, const void* k, int dtype,
@@ -70,6 +80,12 @@ int launch_sampled_retained(const Stage1Geom& g, int exact_all, const int* resco
 // Guard logit bound per (head, chunk): max ||q_r|| * max ||k_j|| / sqrt(d) (bf16 inputs).
 int launch_logit_bound(const Stage1Geom& g, const void* q, const void* k, char* ws, const Workspace& L,
                        double* bound, cudaStream_t st);
+// Band refinement of the selection guard: exact (fp64) masses of the blocks in
+// each recorded band, normalised with the tensor-core row statistics, written
+// over those blocks' col / slash scores; marks band_pairs.
+int launch_refine_bands(const Stage1Geom& g, const void* q, const void* k, int dtype, const int* band,
+                        const int* flags, int* band_pairs, char* ws, const Workspace& L, double* col,
+                        double* slash, cudaStream_t st);
 int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const int* only_flags,
                      char* ws, const Workspace& L, double* col, double* slash, cudaStream_t st);
 // rows' global max / sum, fold into part3, scatter into col / slash.  With

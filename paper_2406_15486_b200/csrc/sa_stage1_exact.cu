@@ -220,7 +220,137 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Exact partials of an explicit (pair, key block) work list (band refinement).
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    xf_items(const T* __restrict__ q, const T* __restrict__ k, Stage1Geom g, const int* __restrict__ items,
+             double* __restrict__ pa, double* __restrict__ pb, double* __restrict__ pm) {
+  extern __shared__ double smem_d[];
+  T* qs = reinterpret_cast<T*>(smem_d);
+  double* ks = reinterpret_cast<double*>(reinterpret_cast<char*>(smem_d) + kRows * kPitchQ * sizeof(T));
+  const int n = items[0];
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {  // uniform per CTA
+    const int hc = items[1 + 2 * i], kb = items[2 + 2 * i];
+    xf_work(q, k, g, hc, kb, kb + 1, pa, pb, pm, qs, ks);
+    __syncthreads();
+  }
+}
+
+// Band entry -> (pair, key block) work items: a col band lists key blocks, a
+// slash band lists offset bins o, each read from key blocks X - o (keys at or
+// below the row's own offset in its block) and X - o - 1 for the query
+// block(s) X the sampled window spans.  Entries of pairs already flagged for
+// the full re-score are skipped.
+__global__ void k_band_items(Stage1Geom g, const int* __restrict__ band, const int* __restrict__ flags,
+                             int* __restrict__ band_pairs, int* __restrict__ items) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= g.Hq * g.cn * 2) return;
+  const int hc = e >> 1, dir = e & 1;
+  const int* ent = band + (size_t)e * kBandEntry;
+  const int n = ent[0];
+  if (n <= 0 || flags[hc]) return;
+  band_pairs[hc] = 1;
+  const Win w = window_of(hc % g.cn, g.S, g.blk, g.itv);
+  const int X0 = w.ss / g.blk, X1 = (w.se - 1) / g.blk;
+  int kbs[kBandItemsPerEntry];
+  int m = 0;
+  auto add = [&](int kb) {
+    if (kb < 0 || kb >= w.nkb) return;
+    for (int i = 0; i < m; ++i)
+      if (kbs[i] == kb) return;
+    kbs[m++] = kb;
+  };
+  for (int i = 0; i < n; ++i) {
+    const int b = ent[2 + i];
+    if (dir == 0) {
+      add(b);
+    } else {
+      for (int X = X0; X <= X1; ++X) {
+        add(X - b);
+        add(X - b - 1);
+      }
+    }
+  }
+  const int at = atomicAdd(items, m);
+  for (int i = 0; i < m; ++i) {
+    items[1 + 2 * (at + i)] = hc;
+    items[2 + 2 * (at + i)] = kbs[i];
+  }
+}
+
+// Refined band scores: per band block, the sum over the window's rows of the
+// exact (fp64) mass in the block / bin, normalised with the tensor-core row
+// statistics (M in log2 units, L): s = sum_r part_r * exp(m_r - M_r ln2) / L_r.
+// Rows are added in a fixed order (deterministic).  Overwrites col / slash.
+__global__ void k_band_scores(Stage1Geom g, const int* __restrict__ band, const int* __restrict__ flags,
+                              const double* __restrict__ xa, const double* __restrict__ xb,
+                              const double* __restrict__ xm, const double* __restrict__ rowstat,
+                              double* __restrict__ col, double* __restrict__ slash) {
+  const int e = blockIdx.x, hc = e >> 1, dir = e & 1;
+  const int* ent = band + (size_t)e * kBandEntry;
+  const int n = ent[0];
+  if (n <= 0 || flags[hc]) return;
+  __shared__ double part[kRows];
+  const Win w = window_of(hc % g.cn, g.S, g.blk, g.itv);
+  const int nr = w.se - w.ss, r = threadIdx.x;
+  double M = 0.0, invL = 0.0;
+  int X = 0;
+  if (r < nr) {
+    const size_t ro = (size_t)hc * g.blk + r;
+    M = rowstat[ro * 2] * 0.6931471805599453;
+    invL = 1.0 / rowstat[ro * 2 + 1];
+    X = (w.ss + r) / g.blk;
+  }
+  auto plane = [&](const double* pl, int kb) -> double {  // exact part of (row r, key block kb), normalised
+    if (kb < 0 || kb >= w.nkb) return 0.0;
+    const size_t o = ((size_t)hc * g.blk + r) * g.nb + kb;
+    const double m = xm[o];
+    return m == -INFINITY ? 0.0 : pl[o] * exp(m - M) * invL;
+  };
+  for (int i = 0; i < n; ++i) {
+    const int b = ent[2 + i];
+    double v = 0.0;
+    if (r < nr) v = dir == 0 ? plane(xa, b) + plane(xb, b) : plane(xa, X - b) + plane(xb, X - b - 1);
+    part[r] = v;
+    __syncthreads();
+    if (r == 0) {
+      double acc = 0.0;
+      for (int t = 0; t < nr; ++t) acc += part[t];
+      (dir == 0 ? col : slash)[(size_t)hc * g.nb + b] = acc;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+int launch_refine_bands(const Stage1Geom& g, const void* q, const void* k, int dtype, const int* band,
+                        const int* flags, int* band_pairs, char* ws, const Workspace& L, double* col,
+                        double* slash, cudaStream_t st) {
+  int* items = reinterpret_cast<int*>(ws + L.band_items);
+  const int n_ent = g.Hq * g.cn * 2;
+  cudaMemsetAsync(items, 0, sizeof(int), st);
+  cudaMemsetAsync(band_pairs, 0, sizeof(int) * g.Hq * g.cn, st);
+  k_band_items<<<ceil_div(n_ent, 128), 128, 0, st>>>(g, band, flags, band_pairs, items);
+  if (int e = check_launch("band refinement: work list")) return e;
+  const size_t plane = (size_t)g.Hq * g.cn * g.blk * g.nb;
+  double* pa = reinterpret_cast<double*>(ws + L.x_part);
+  double* pb = pa + plane;
+  double* pm = pb + plane;
+  if (dtype == SA_FP32) {
+    set_smem_attr(reinterpret_cast<const void*>(&xf_items<float>), xf_smem_bytes<float>());
+    xf_items<float><<<2 * 148, kThreads, xf_smem_bytes<float>(), st>>>(
+        static_cast<const float*>(q), static_cast<const float*>(k), g, items, pa, pb, pm);
+  } else {
+    set_smem_attr(reinterpret_cast<const void*>(&xf_items<__nv_bfloat16>), xf_smem_bytes<__nv_bfloat16>());
+    xf_items<__nv_bfloat16><<<2 * 148, kThreads, xf_smem_bytes<__nv_bfloat16>(), st>>>(
+        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k), g, items, pa, pb, pm);
+  }
+  if (int e = check_launch("band refinement: exact partials")) return e;
+  k_band_scores<<<n_ent, kRows, 0, st>>>(g, band, flags, pa, pb, pm,
+                                         reinterpret_cast<const double*>(ws + L.rowstat), col, slash);
+  return check_launch("band refinement: scores");
+}
 
 // Per sampled row: global max M and normaliser L over the row's key blocks.
 // One warp per row, lanes stride the key blocks; fixed shuffle tree.

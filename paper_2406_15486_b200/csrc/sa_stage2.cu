@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kSelThreads)
               int npow2, double alpha_c, double alpha_s, double eps, const double* __restrict__ bound,
               double bound_ref, int* __restrict__ flags,
               const int* __restrict__ only, const int* __restrict__ k_in, int* __restrict__ k_out,
-              int* __restrict__ idx_out) {
+              int* __restrict__ idx_out, int* __restrict__ band) {
   extern __shared__ unsigned char smem_raw[];
   const int dir = blockIdx.x, hc = blockIdx.y;
   if (only && only[hc] == 0) return;
@@ -106,17 +106,42 @@ __global__ void __launch_bounds__(kSelThreads)
     if (k_in) k = min(max(k_in[hc * 2 + dir], 0), nb);
     s_k = k;
     k_out[hc * 2 + dir] = k;
+    const double scale_b = bound ? fmax(1.0, bound[hc] / bound_ref) : 1.0;
+    auto sc = [&](int i) { return __longlong_as_double((long long)key[i]); };
+    int* ent = band ? band + ((size_t)hc * 2 + dir) * kBandEntry : nullptr;
+    if (ent && !k_in) ent[0] = 0;
     if (eps > 0.0 && k > 0 && flags && !k_in) {
-      // margin widened for large-logit pairs (bound: see k_pair_bound, sa_stage1_tc.cu)
-      const double E = eps * total * (bound ? fmax(1.0, bound[hc] / bound_ref) : 1.0);
-      bool close = (cum[k - 1] - target) < E;
-      if (k >= 2 && (target - cum[k - 2]) < E) close = true;
-      if (k < nb) {
-        const double a = __longlong_as_double((long long)key[k - 1]);
-        const double b = __longlong_as_double((long long)key[k]);
-        if (a - b < E) close = true;
+      // guard: margin widened for large-logit pairs (bound: see k_pair_bound, sa_stage1_tc.cu)
+      const double E = eps * total * scale_b;
+      const double m1 = cum[k - 1] - target, m2 = k >= 2 ? target - cum[k - 2] : INFINITY;
+      const bool cut = m1 < E || m2 < E;
+      const bool tie = k < nb && sc(k - 1) - sc(k) < E;
+      if (cut) {
+        atomicOr(flags + hc, 1);
+      } else if (tie) {
+        // A boundary tie alone decides only WHICH of a few nearly equal blocks
+        // make the cut: the run of blocks around ranks k-1, k whose consecutive
+        // gaps are below 2E (every block outside it is ordered against it by
+        // more than the error) goes to the band refinement, provided k itself
+        // is safe from swaps inside the run; else the whole pair is re-scored.
+        int lo = k - 1, hi = k;
+        while (lo > 0 && sc(lo - 1) - sc(lo) < 2.0 * E) --lo;
+        while (hi + 1 < nb && sc(hi) - sc(hi + 1) < 2.0 * E) ++hi;
+        const double spread = sc(lo) - sc(hi);
+        if (!ent || hi - lo + 1 > kBandMax || m1 < E + spread || m2 < E + spread) {
+          atomicOr(flags + hc, 1);
+        } else {
+          ent[0] = hi - lo + 1;
+          ent[1] = lo;
+          for (int i = lo; i <= hi; ++i) ent[2 + i - lo] = idx[i];
+        }
       }
-      if (close) atomicOr(flags + hc, 1);
+    } else if (eps > 0.0 && k > 0 && flags && k_in && k < nb) {
+      // band certification (k from the guard pass, refined scores): the two
+      // blocks at the cut must differ by more than the refinement's error
+      // bound, eps * (s_a + s_b) (row-normaliser error, scaled like the guard)
+      const double a = sc(k - 1), b = sc(k);
+      if (!(a - b > eps * scale_b * (a + b))) atomicOr(flags + hc, 1);
     }
   }
   __syncthreads();
@@ -393,7 +418,7 @@ __global__ void k_check_finite(const uint32_t* __restrict__ x, long long nwords,
 
 int launch_select(const double* col, const double* slash, int Hq, int cn, int nb, double ac,
                   double as, double eps, const double* bound, double bound_ref, int* flags, const int* only,
-                  const int* k_in, int* k_out, int* idx_out, cudaStream_t st) {
+                  const int* k_in, int* k_out, int* idx_out, int* band, cudaStream_t st) {
   int npow2 = 1;
   while (npow2 < nb) npow2 <<= 1;
   const size_t smem = (size_t)npow2 * (8 + 8 + 4 + 1);
@@ -401,7 +426,7 @@ int launch_select(const double* col, const double* slash, int Hq, int cn, int nb
   cudaFuncSetAttribute(k2_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int threads = npow2 >= 2048 ? 1024 : (npow2 >= 64 ? npow2 / 2 : 32);
   k2_select<<<dim3(2, Hq * cn), threads, smem, st>>>(col, slash, cn, nb, npow2, ac, as, eps, bound, bound_ref, flags,
-                                                     only, k_in, k_out, idx_out);
+                                                     only, k_in, k_out, idx_out, band);
   return check_launch("sa_select");
 }
 

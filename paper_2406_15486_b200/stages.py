@@ -50,6 +50,13 @@ GUARD_EPS = 4e-7
 # margin grows in proportion, keeping it >= 2.6x the worst measured error at
 # every B.
 GUARD_LOGIT_REF = 320.0
+# Band refinement: the refined scores of tied blocks carry the relative error of
+# stage 1's tensor-core row normalisers (tools/rownorm_diag.py: <= 5.2e-6 at C3 /
+# C4 10 %, profiles/r2/rownorm_*.txt), scaled like GUARD_EPS with the logit
+# bound; the cut between two refined scores is trusted when they differ by more
+# than BAND_EPS * (s_a + s_b) (~6x the worst measured error), else the pair is
+# re-scored in full.
+BAND_EPS = 3e-5
 
 _WS_CACHE: dict = {}
 
@@ -203,7 +210,7 @@ def _vector_select(scores, alpha, k=None):
     if k is not None:
         k_in = torch.tensor([[[k, k]]], dtype=torch.int32, device=dev)
     dcall(dev, "sa_select", t.data_ptr(), t.data_ptr(), 1, 1, s.size, alpha, alpha, 0.0, None, 1.0, None, None,
-              None if k_in is None else k_in.data_ptr(), k_out.data_ptr(), idx.data_ptr(),
+              None if k_in is None else k_in.data_ptr(), k_out.data_ptr(), idx.data_ptr(), None,
               torch.cuda.current_stream(dev).cuda_stream)
     kk = int(k_out[0, 0, 0].item())
     return kk, tuple(int(x) for x in idx[0, 0, 0, :kk].cpu().numpy())
@@ -240,11 +247,18 @@ def arg_topk(scores, k: int) -> tuple:
 class Selection:
     k_sel: torch.Tensor     # int32 [H, cn, 2]
     idx_sel: torch.Tensor   # int32 [H, cn, 2, nb]
-    flags: torch.Tensor | None = None  # int32 [H*cn]: pairs the guard re-scored
+    flags: torch.Tensor | None = None  # int32 [H*cn]: pairs the guard re-scored in full (fp64)
     guard: str = "auto"
+    band_pairs: torch.Tensor | None = None  # int32 [H*cn]: pairs whose tie band was refined
 
     def n_rescored(self) -> int:
         return 0 if self.flags is None else int(self.flags.sum().item())
+
+    def n_band_refined(self) -> int:
+        """Pairs settled by the band refinement alone (not re-scored in full)."""
+        if self.band_pairs is None:
+            return 0
+        return int(((self.band_pairs != 0) & (self.flags == 0)).sum().item())
 
 
 def select(reduced: ReducedScores, cfg: SparseConfig, guard: str = "auto",
@@ -265,15 +279,30 @@ def select(reduced: ReducedScores, cfg: SparseConfig, guard: str = "auto",
     use_guard = guard == "auto" and reduced.mode == "tensor"
     flags = torch.zeros(H * cn, dtype=torch.int32, device=dev) if use_guard else None
     bound = reduced.logit_bound if use_guard else None
-    dcall(dev, "sa_select", reduced.col.data_ptr(), reduced.slash.data_ptr(), H, cn, nb, cfg.alpha_c,
-          cfg.alpha_s, guard_eps if use_guard else 0.0, None if bound is None else bound.data_ptr(),
-          GUARD_LOGIT_REF, None if flags is None else flags.data_ptr(), None, None, k_sel.data_ptr(),
-          idx_sel.data_ptr(), st)
+    band = band_pairs = None
     if use_guard:
+        band = torch.empty(_lib.load().sa_band_table_len(H, cn), dtype=torch.int32, device=dev)
+        band_pairs = torch.empty(H * cn, dtype=torch.int32, device=dev)
+    col, slash = reduced.col.data_ptr(), reduced.slash.data_ptr()
+    dcall(dev, "sa_select", col, slash, H, cn, nb, cfg.alpha_c, cfg.alpha_s, guard_eps if use_guard else 0.0,
+          None if bound is None else bound.data_ptr(), GUARD_LOGIT_REF, None if flags is None else flags.data_ptr(),
+          None, None, k_sel.data_ptr(), idx_sel.data_ptr(), None if band is None else band.data_ptr(), st)
+    if use_guard:
+        # boundary ties alone: exact scores of the few tied blocks, then a
+        # re-select with the guard's k that certifies the refined cut (else the
+        # pair joins the full re-score)
+        ws = _workspace(b, plan.blk, plan.chunk_n)
+        dcall(dev, "sa_refine_bands", b.q.data_ptr(), b.k.data_ptr(), b.dtype_code, b.S, b.Hq, b.Hkv, b.d, plan.blk,
+              b.group, b.q_head0, plan.chunk_n, plan.itv, band.data_ptr(), flags.data_ptr(), band_pairs.data_ptr(),
+              col, slash, ws.data_ptr(), ws.numel(), st)
+        dcall(dev, "sa_select", col, slash, H, cn, nb, cfg.alpha_c, cfg.alpha_s, BAND_EPS, bound.data_ptr(),
+              GUARD_LOGIT_REF, flags.data_ptr(), band_pairs.data_ptr(), k_sel.data_ptr(), k_sel.data_ptr(),
+              idx_sel.data_ptr(), None, st)
+        # everything else the guard flagged: the exact (fp64) stage 1 of the pair, then a fresh selection
         _stage1(b, plan, reduced.col, reduced.slash, _lib.SA_STAGE1_EXACT, only=flags)
-        dcall(dev, "sa_select", reduced.col.data_ptr(), reduced.slash.data_ptr(), H, cn, nb, cfg.alpha_c,
-              cfg.alpha_s, 0.0, None, 1.0, None, flags.data_ptr(), None, k_sel.data_ptr(), idx_sel.data_ptr(), st)
-    return Selection(k_sel, idx_sel, flags, guard)
+        dcall(dev, "sa_select", col, slash, H, cn, nb, cfg.alpha_c, cfg.alpha_s, 0.0, None, 1.0, None,
+              flags.data_ptr(), None, k_sel.data_ptr(), idx_sel.data_ptr(), None, st)
+    return Selection(k_sel, idx_sel, flags, guard, band_pairs)
 
 
 def _selection_from_indices(selected, n_chunks: int, nb: int, device) -> Selection:
