@@ -25,7 +25,16 @@ namespace sa {
 namespace {
 
 constexpr int kThreads = 192;  // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 softmax
-constexpr int kStages = 2;
+#ifndef SA_K1_CTAS
+#define SA_K1_CTAS 3
+#endif
+// 3 CTAs per SM, each with a single K stage and a single TMEM S (smem 64 KB,
+// 128 TMEM columns): the other CTAs' work fills the gaps of a CTA's
+// load -> QK^T -> softmax chain (C3 stage-1 kernel -4 %, C4 -1.5 % against 2
+// CTAs with a 2-stage ring and a double-buffered S, profiles/r2/k1_ctas_ab.txt)
+constexpr int kCtasPerSm = SA_K1_CTAS;
+constexpr int kStages = kCtasPerSm >= 3 ? 1 : 2;
+constexpr int kSBuf = kCtasPerSm >= 3 ? 1 : 2;
 constexpr uint32_t kTileBytes = 128 * 128 * 2;  // one 128 x 128 bf16 tile (two 64-col boxes)
 constexpr uint32_t kBoxBytes = kTileBytes / 2;
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, false);
@@ -48,7 +57,7 @@ struct K1Params {
   float* pm;
 };
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     k1_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
           const K1Params P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -86,14 +95,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(&sm->k_full[i], 1);
       mbar_init(&sm->k_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSBuf; ++i) {
       mbar_init(&sm->s_full[i], 1);
       mbar_init(&sm->s_empty[i], 128);
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    tmem_alloc(&sm->tmem_base, 256);
+    tmem_alloc(&sm->tmem_base, 128 * kSBuf);
     tmem_relinquish();
   }
   tc_fence_before();
@@ -120,9 +129,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_wait(&sm->q_full, 0);
     const uint32_t q_addr = smem_u32(sQ);
     for (int j = 0; j < n; ++j) {
-      const int st = j % kStages, buf = j & 1;
+      const int st = j % kStages, buf = j % kSBuf;
       mbar_wait(&sm->k_full[st], (j / kStages) & 1);
-      if (j >= 2) mbar_wait(&sm->s_empty[buf], ((j >> 1) - 1) & 1);
+      if (j >= kSBuf) mbar_wait(&sm->s_empty[buf], ((j / kSBuf) - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t k_addr = smem_u32(sK + st * kTileBytes);
@@ -148,9 +157,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     float m_run = -INFINITY;
     const size_t prow = ((size_t)hc * 128 + rl) * g.nb;
     for (int j = 0; j < n; ++j) {
-      const int buf = j & 1;
+      const int buf = j % kSBuf;
       const int kb = kb0 + j;
-      mbar_wait(&sm->s_full[buf], (j >> 1) & 1);
+      mbar_wait(&sm->s_full[buf], (j / kSBuf) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * 128;
       const int lim = row - kb * 128;  // keys t <= lim are causal
@@ -226,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, 128 * kSBuf);
   }
 }
 
@@ -334,7 +343,7 @@ int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const in
   P.pm = P.pb + plane;
   // split the key range so the grid covers the SMs a few times over
   const long long total_kb = (long long)g.Hq * g.cn * g.nb;
-  int kpc = (int)std::max<long long>(4, std::min<long long>(64, total_kb / (148LL * 2 * 4)));
+  int kpc = (int)std::max<long long>(4, std::min<long long>(64, total_kb / (148LL * kCtasPerSm * 4)));
   P.kb_per_cta = kpc;
   const int nsplit = ceil_div(g.nb, kpc);
   const size_t smem = kTileBytes * (1 + kStages) + sizeof(K1Smem) + 1024;
