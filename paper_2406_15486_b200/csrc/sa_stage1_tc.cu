@@ -25,16 +25,13 @@ namespace sa {
 namespace {
 
 constexpr int kThreads = 192;  // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 softmax
-#ifndef SA_K1_CTAS
-#define SA_K1_CTAS 3
-#endif
 // 3 CTAs per SM, each with a single K stage and a single TMEM S (smem 64 KB,
 // 128 TMEM columns): the other CTAs' work fills the gaps of a CTA's
 // load -> QK^T -> softmax chain (C3 stage-1 kernel -4 %, C4 -1.5 % against 2
 // CTAs with a 2-stage ring and a double-buffered S, profiles/r2/k1_ctas_ab.txt)
-constexpr int kCtasPerSm = SA_K1_CTAS;
-constexpr int kStages = kCtasPerSm >= 3 ? 1 : 2;
-constexpr int kSBuf = kCtasPerSm >= 3 ? 1 : 2;
+constexpr int kCtasPerSm = 3;
+constexpr int kStages = 1;  // K ring depth
+constexpr int kSBuf = 1;    // TMEM S buffers
 constexpr uint32_t kTileBytes = 128 * 128 * 2;  // one 128 x 128 bf16 tile (two 64-col boxes)
 constexpr uint32_t kBoxBytes = kTileBytes / 2;
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, false);
