@@ -4,9 +4,9 @@
 //
 // One CTA = (q head h, chunk c, key-block split).  The chunk's 128 sampled
 // query rows (a possibly UNALIGNED window, sampler.py:103-117) are TMA-loaded
-// once; key tiles stream through a 2-stage TMA ring; S = Q K^T is computed by
-// tcgen05.mma into a double-buffered TMEM accumulator (2 x 128 columns) so
-// the MMA of tile j+1 overlaps the softmax of tile j.  Four softmax warps own
+// once; key tiles stream through TMA; S = Q K^T is computed by tcgen05.mma into
+// a TMEM accumulator (128 columns); three CTAs share an SM, so one CTA's MMA
+// and loads overlap the others' softmax.  Four softmax warps own
 // one sampled row each per thread (TMEM lane == row) and, per key block, emit
 // the row's running log2-max m and the two partial masses
 //     A = sum_{t <= r%128} exp2(s - m),   B = sum_{t > r%128} exp2(s - m)
