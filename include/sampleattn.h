@@ -108,25 +108,28 @@ int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, i
 
 /* Stage 2a — replaces find_k + arg_topk per (head, chunk, direction)
  * (filtering.py:30-62, applied as in select_and_merge :245-255).
- * margin_eps > 0 (with k_in == NULL) enables the selection guard.  E =
- * margin_eps * max(1, logit_bound[hc] / bound_ref) * total is the error the
- * scores of pair hc may carry (logit_bound from sa_stage1, may be NULL):
+ * margin_eps > 0 enables the selection guard.  E = margin_eps *
+ * max(1, logit_bound[hc] / bound_ref) * total is the error the tensor-core
+ * scores of pair hc may carry (logit_bound from sa_stage1, may be NULL).
+ * Guard pass (band != NULL or NULL, only_flags == NULL):
  *   - alpha cut within E of a decision (either side): flags[hc] = 1 (the
  *     pair needs its exact re-score);
- *   - only the boundary tie within E: the run of blocks around the cut whose
- *     consecutive gaps are below 2E is recorded in band (sa_band_table_len
- *     ints: per (hc, dir) [count, first rank, block / bin indices]) for
- *     sa_refine_bands -- or flags[hc] = 1 when band is NULL, the run is longer
- *     than 16 blocks, or the cut margins do not cover swaps inside it.
- * margin_eps > 0 WITH k_in certifies refined scores: flags[hc] = 1 when the
- * two blocks at the cut differ by less than margin_eps * (scale) * (s_a + s_b).
+ *   - only the boundary tie within E: the blocks whose scores lie within 2E
+ *     of the k-th largest are recorded in band (sa_band_table_len ints: per
+ *     (hc, dir) [count, first rank, block / bin indices]) for
+ *     sa_refine_bands -- or flags[hc] = 1 when band is NULL or they are more
+ *     than 64.
+ * Certify pass (band != NULL and only_flags != NULL, after sa_refine_bands):
+ * k is recomputed on the refined scores and flags[hc] = 1 unless the alpha
+ * cut clears E on both sides and the two blocks at the cut differ by more
+ * than band_eps * (scale) * (s_a + s_b) (both refined) or E (otherwise).
  * only_flags != NULL recomputes the flagged pairs only.  k_in != NULL
  * ([Hq][cn][2]) skips find_k and takes the given k (the reference's
  * arg_topk(scores, k), filtering.py:51-62). */
 int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int nb,
               double alpha_c, double alpha_s, double margin_eps, const double* logit_bound,
               double bound_ref, int* flags, const int* only_flags, const int* k_in, int* k_out,
-              int* idx_out, int* band, void* stream);
+              int* idx_out, int* band, double band_eps, void* stream);
 
 /* Selection guard, band refinement (no reference counterpart: it reproduces the
  * reference's fp64 ordering of the few nearly tied blocks at a cut).  For each

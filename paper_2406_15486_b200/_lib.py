@@ -36,7 +36,7 @@ SIGNATURES = {
     "sa_check_finite": (_I, [_P, _I, ctypes.c_int64, _P, _P]),
     "sa_copy2d_async": (_I, [_P, ctypes.c_size_t, _P, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, _P]),
     "sa_stage1": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _Z, _P]),
-    "sa_select": (_I, [_P, _P, _I, _I, _I, _D, _D, _D, _P, _D, _P, _P, _P, _P, _P, _P, _P]),
+    "sa_select": (_I, [_P, _P, _I, _I, _I, _D, _D, _D, _P, _D, _P, _P, _P, _P, _P, _P, _D, _P]),
     "sa_band_table_len": (_I, [_I, _I]),
     "sa_refine_bands": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "sa_merge": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),

@@ -23,7 +23,7 @@ namespace sa {
 
 int launch_select(const double* col, const double* slash, int Hq, int cn, int nb, double ac,
                   double as, double eps, const double* bound, double bound_ref, int* flags, const int* only,
-                  const int* k_in, int* k_out, int* idx_out, int* band, cudaStream_t st);
+                  const int* k_in, int* k_out, int* idx_out, int* band, double band_eps, cudaStream_t st);
 int launch_merge(const int* k_sel, const int* idx_sel, int Hq, int cn, int nb, int S, int blk,
                  int itv, int sink_blocks, int local_blocks, int* kv_cnt, int* kv_idx,
                  long long* ab, long long* ae, cudaStream_t st);
@@ -231,7 +231,8 @@ int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, i
 
 int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int nb, double alpha_c,
               double alpha_s, double margin_eps, const double* logit_bound, double bound_ref, int* flags,
-              const int* only_flags, const int* k_in, int* k_out, int* idx_out, int* band, void* stream) {
+              const int* only_flags, const int* k_in, int* k_out, int* idx_out, int* band, double band_eps,
+              void* stream) {
   if (!(alpha_c >= 0.0 && alpha_c <= 1.0))
     return fail(SA_ERR_INVALID, "alpha_c must be in [0, 1]");
   if (!(alpha_s >= 0.0 && alpha_s <= 1.0))
@@ -241,7 +242,7 @@ int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int n
   if (margin_eps > 0.0 && !flags) return fail(SA_ERR_INVALID, "sa_select: guard needs flags");
   if (logit_bound && !(bound_ref > 0.0)) return fail(SA_ERR_INVALID, "sa_select: bound_ref must be > 0");
   return launch_select(col, slash, Hq, chunk_n, nb, alpha_c, alpha_s, margin_eps, logit_bound, bound_ref, flags,
-                       only_flags, k_in, k_out, idx_out, band, static_cast<cudaStream_t>(stream));
+                       only_flags, k_in, k_out, idx_out, band, band_eps, static_cast<cudaStream_t>(stream));
 }
 
 int sa_band_table_len(int Hq, int chunk_n) {

@@ -61,7 +61,7 @@ Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int d
 
 // Selection guard, band refinement: per (head, chunk, direction) the run of
 // nearly tied blocks at the cut -- [count, first rank, block / bin indices].
-constexpr int kBandMax = 16;
+constexpr int kBandMax = 64;
 constexpr int kBandEntry = 2 + kBandMax;
 
 // key blocks one band entry can need: a slash bin reads two key blocks for each

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kSelThreads)
               int npow2, double alpha_c, double alpha_s, double eps, const double* __restrict__ bound,
               double bound_ref, int* __restrict__ flags,
               const int* __restrict__ only, const int* __restrict__ k_in, int* __restrict__ k_out,
-              int* __restrict__ idx_out, int* __restrict__ band) {
+              int* __restrict__ idx_out, int* __restrict__ band, double band_eps) {
   extern __shared__ unsigned char smem_raw[];
   const int dir = blockIdx.x, hc = blockIdx.y;
   if (only && only[hc] == 0) return;
@@ -109,39 +109,52 @@ __global__ void __launch_bounds__(kSelThreads)
     const double scale_b = bound ? fmax(1.0, bound[hc] / bound_ref) : 1.0;
     auto sc = [&](int i) { return __longlong_as_double((long long)key[i]); };
     int* ent = band ? band + ((size_t)hc * 2 + dir) * kBandEntry : nullptr;
-    if (ent && !k_in) ent[0] = 0;
-    if (eps > 0.0 && k > 0 && flags && !k_in) {
-      // guard: margin widened for large-logit pairs (bound: see k_pair_bound, sa_stage1_tc.cu)
-      const double E = eps * total * scale_b;
+    const bool certify = band && only;  // re-select of refined pairs
+    const double E = eps * total * scale_b;  // error bound of tensor-core scores (guard)
+    if (ent && !certify) ent[0] = 0;
+    if (eps > 0.0 && k > 0 && flags && !k_in && !certify) {
+      // guard pass: margin widened for large-logit pairs (bound: see k_pair_bound, sa_stage1_tc.cu)
       const double m1 = cum[k - 1] - target, m2 = k >= 2 ? target - cum[k - 2] : INFINITY;
       const bool cut = m1 < E || m2 < E;
       const bool tie = k < nb && sc(k - 1) - sc(k) < E;
       if (cut) {
         atomicOr(flags + hc, 1);
       } else if (tie) {
-        // A boundary tie alone decides only WHICH of a few nearly equal blocks
-        // make the cut: the run of blocks around ranks k-1, k whose consecutive
-        // gaps are below 2E (every block outside it is ordered against it by
-        // more than the error) goes to the band refinement, provided k itself
-        // is safe from swaps inside the run; else the whole pair is re-scored.
-        int lo = k - 1, hi = k;
-        while (lo > 0 && sc(lo - 1) - sc(lo) < 2.0 * E) --lo;
-        while (hi + 1 < nb && sc(hi) - sc(hi + 1) < 2.0 * E) ++hi;
-        const double spread = sc(lo) - sc(hi);
-        if (!ent || hi - lo + 1 > kBandMax || m1 < E + spread || m2 < E + spread) {
+        // A boundary tie alone leaves only WHICH blocks make the cut in doubt.
+        // With every score within E of its exact value, the exact k-th largest
+        // score lies within E of hi = s(k-1): blocks above hi + 2E are in,
+        // blocks below hi - 2E are out, and the band between (contiguous in
+        // sorted order) goes to the refinement; else the pair is re-scored.
+        const double hi = sc(k - 1);
+        int a = k - 1, z = k - 1;
+        while (a > 0 && sc(a - 1) <= hi + 2.0 * E) --a;
+        while (z + 1 < nb && sc(z + 1) >= hi - 2.0 * E) ++z;
+        if (!ent || z - a + 1 > kBandMax) {
           atomicOr(flags + hc, 1);
         } else {
-          ent[0] = hi - lo + 1;
-          ent[1] = lo;
-          for (int i = lo; i <= hi; ++i) ent[2 + i - lo] = idx[i];
+          ent[0] = z - a + 1;
+          ent[1] = a;
+          for (int i = a; i <= z; ++i) ent[2 + i - a] = idx[i];
         }
       }
-    } else if (eps > 0.0 && k > 0 && flags && k_in && k < nb) {
-      // band certification (k from the guard pass, refined scores): the two
-      // blocks at the cut must differ by more than the refinement's error
-      // bound, eps * (s_a + s_b) (row-normaliser error, scaled like the guard)
-      const double a = sc(k - 1), b = sc(k);
-      if (!(a - b > eps * scale_b * (a + b))) atomicOr(flags + hc, 1);
+    } else if (certify && eps > 0.0 && k > 0 && flags && ent) {
+      // certify a refined pair: band blocks now carry near-exact scores, the
+      // others tensor-core ones (error <= E, which also bounds the prefix
+      // sums), so k must clear the alpha cut by E on both sides, and the two
+      // blocks at the cut must differ by more than their own error: the
+      // refinement's band_eps * (s_a + s_b) when both are refined, E otherwise
+      const double m1 = cum[k - 1] - target, m2 = k >= 2 ? target - cum[k - 2] : INFINITY;
+      bool ok = m1 >= E && m2 >= E;
+      if (ok && k < nb) {
+        const double sa = sc(k - 1), sb = sc(k);
+        bool ra = false, rb = false;
+        for (int i = 0; i < ent[0]; ++i) {
+          ra |= ent[2 + i] == idx[k - 1];
+          rb |= ent[2 + i] == idx[k];
+        }
+        ok = (ra && rb) ? sa - sb > band_eps * scale_b * (sa + sb) : sa - sb >= E;
+      }
+      if (!ok) atomicOr(flags + hc, 1);
     }
   }
   __syncthreads();
@@ -418,7 +431,7 @@ __global__ void k_check_finite(const uint32_t* __restrict__ x, long long nwords,
 
 int launch_select(const double* col, const double* slash, int Hq, int cn, int nb, double ac,
                   double as, double eps, const double* bound, double bound_ref, int* flags, const int* only,
-                  const int* k_in, int* k_out, int* idx_out, int* band, cudaStream_t st) {
+                  const int* k_in, int* k_out, int* idx_out, int* band, double band_eps, cudaStream_t st) {
   int npow2 = 1;
   while (npow2 < nb) npow2 <<= 1;
   const size_t smem = (size_t)npow2 * (8 + 8 + 4 + 1);
@@ -426,7 +439,7 @@ int launch_select(const double* col, const double* slash, int Hq, int cn, int nb
   cudaFuncSetAttribute(k2_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int threads = npow2 >= 2048 ? 1024 : (npow2 >= 64 ? npow2 / 2 : 32);
   k2_select<<<dim3(2, Hq * cn), threads, smem, st>>>(col, slash, cn, nb, npow2, ac, as, eps, bound, bound_ref, flags,
-                                                     only, k_in, k_out, idx_out, band);
+                                                     only, k_in, k_out, idx_out, band, band_eps);
   return check_launch("sa_select");
 }
 

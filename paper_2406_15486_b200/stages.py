@@ -210,7 +210,7 @@ def _vector_select(scores, alpha, k=None):
     if k is not None:
         k_in = torch.tensor([[[k, k]]], dtype=torch.int32, device=dev)
     dcall(dev, "sa_select", t.data_ptr(), t.data_ptr(), 1, 1, s.size, alpha, alpha, 0.0, None, 1.0, None, None,
-              None if k_in is None else k_in.data_ptr(), k_out.data_ptr(), idx.data_ptr(), None,
+              None if k_in is None else k_in.data_ptr(), k_out.data_ptr(), idx.data_ptr(), None, 0.0,
               torch.cuda.current_stream(dev).cuda_stream)
     kk = int(k_out[0, 0, 0].item())
     return kk, tuple(int(x) for x in idx[0, 0, 0, :kk].cpu().numpy())
@@ -286,22 +286,22 @@ def select(reduced: ReducedScores, cfg: SparseConfig, guard: str = "auto",
     col, slash = reduced.col.data_ptr(), reduced.slash.data_ptr()
     dcall(dev, "sa_select", col, slash, H, cn, nb, cfg.alpha_c, cfg.alpha_s, guard_eps if use_guard else 0.0,
           None if bound is None else bound.data_ptr(), GUARD_LOGIT_REF, None if flags is None else flags.data_ptr(),
-          None, None, k_sel.data_ptr(), idx_sel.data_ptr(), None if band is None else band.data_ptr(), st)
+          None, None, k_sel.data_ptr(), idx_sel.data_ptr(), None if band is None else band.data_ptr(), 0.0, st)
     if use_guard:
-        # boundary ties alone: exact scores of the few tied blocks, then a
-        # re-select with the guard's k that certifies the refined cut (else the
-        # pair joins the full re-score)
+        # boundary ties alone: exact scores of the blocks within 2E of the cut,
+        # then a re-select that certifies the refined cut (else the pair joins
+        # the full re-score)
         ws = _workspace(b, plan.blk, plan.chunk_n)
         dcall(dev, "sa_refine_bands", b.q.data_ptr(), b.k.data_ptr(), b.dtype_code, b.S, b.Hq, b.Hkv, b.d, plan.blk,
               b.group, b.q_head0, plan.chunk_n, plan.itv, band.data_ptr(), flags.data_ptr(), band_pairs.data_ptr(),
               col, slash, ws.data_ptr(), ws.numel(), st)
-        dcall(dev, "sa_select", col, slash, H, cn, nb, cfg.alpha_c, cfg.alpha_s, BAND_EPS, bound.data_ptr(),
-              GUARD_LOGIT_REF, flags.data_ptr(), band_pairs.data_ptr(), k_sel.data_ptr(), k_sel.data_ptr(),
-              idx_sel.data_ptr(), None, st)
+        dcall(dev, "sa_select", col, slash, H, cn, nb, cfg.alpha_c, cfg.alpha_s, guard_eps, bound.data_ptr(),
+              GUARD_LOGIT_REF, flags.data_ptr(), band_pairs.data_ptr(), None, k_sel.data_ptr(), idx_sel.data_ptr(),
+              band.data_ptr(), BAND_EPS, st)
         # everything else the guard flagged: the exact (fp64) stage 1 of the pair, then a fresh selection
         _stage1(b, plan, reduced.col, reduced.slash, _lib.SA_STAGE1_EXACT, only=flags)
         dcall(dev, "sa_select", col, slash, H, cn, nb, cfg.alpha_c, cfg.alpha_s, 0.0, None, 1.0, None,
-              flags.data_ptr(), None, k_sel.data_ptr(), idx_sel.data_ptr(), None, st)
+              flags.data_ptr(), None, k_sel.data_ptr(), idx_sel.data_ptr(), None, 0.0, st)
     return Selection(k_sel, idx_sel, flags, guard, band_pairs)
 
 

@@ -103,10 +103,10 @@ def test_c_abi_rejects_bad_arguments_without_touching_the_gpu():
                        _lib.SA_STAGE1_TENSOR, None, fake, 1 << 30, None)
     assert rc == _lib.SA_ERR_INVALID and "kv heads" in _err(lib)
     # stage 2: alpha outside [0, 1] (ref sampler.py:52-56), guard without flags
-    assert lib.sa_select(fake, fake, 1, 1, 8, 1.5, 0.9, 0.0, None, 1.0, None, None, None, fake, fake, None, None) == _lib.SA_ERR_INVALID
+    assert lib.sa_select(fake, fake, 1, 1, 8, 1.5, 0.9, 0.0, None, 1.0, None, None, None, fake, fake, None, 0.0, None) == _lib.SA_ERR_INVALID
     assert "alpha_c" in _err(lib)
-    assert lib.sa_select(fake, fake, 1, 1, 8, 0.9, 0.9, 1e-7, None, 1.0, None, None, None, fake, fake, None, None) == _lib.SA_ERR_INVALID
-    assert lib.sa_select(fake, fake, 1, 1, 8, 0.9, 0.9, 1e-7, fake, 0.0, fake, None, None, fake, fake, None, None) \
+    assert lib.sa_select(fake, fake, 1, 1, 8, 0.9, 0.9, 1e-7, None, 1.0, None, None, None, fake, fake, None, 0.0, None) == _lib.SA_ERR_INVALID
+    assert lib.sa_select(fake, fake, 1, 1, 8, 0.9, 0.9, 1e-7, fake, 0.0, fake, None, None, fake, fake, None, 0.0, None) \
         == _lib.SA_ERR_INVALID and "bound_ref" in _err(lib)
     assert lib.sa_merge(fake, fake, 1, 1, 7, 1024, 128, 1024, 0, 1, fake, fake, None, None, None) == _lib.SA_ERR_INVALID
     assert lib.sa_schedule_len(0, 8, 1, 0) < 0

@@ -15,7 +15,11 @@ from paper_2406_15486_b200 import synth  # noqa: E402
 from paper_2406_15486_b200.stages import GUARD_EPS, GUARD_LOGIT_REF  # noqa: E402
 
 S = int(sys.argv[1]); cn = int(sys.argv[2]); Hkv = int(sys.argv[3]); Hq = 32
-q, k, v, _ = synth.make_inputs(S, Hq, Hkv, seed=0, device="cuda")
+if len(sys.argv) > 4 and sys.argv[4] == "ref":  # the reference's calibrated generator (bench --config c2ref)
+    import bench
+    q, k, v, _, _ = bench.workload_inputs("c2ref", S, Hq, Hkv, 128, 0, list(range(Hq)), "cuda")
+else:
+    q, k, v, _ = synth.make_inputs(S, Hq, Hkv, seed=0, device="cuda")
 b = sa.HeadBatch.from_tensors(q, k, v)
 plan = sa.plan_chunks(S, sa.SparseConfig(chunk_n=cn))
 rt = sa.block_reduce(sa.sample_scores(b, plan), 128, mode="tensor")
@@ -36,6 +40,7 @@ def select(s, alpha):
 for alpha in (0.90, 0.95, 0.98):
     n_dec = n_cut = n_tie_only = 0
     bands = []
+    chains = []
     hybrid_ok = 0
     for h in range(Hq):
         for c in range(plan.chunk_n):
@@ -55,6 +60,13 @@ for alpha in (0.90, 0.95, 0.98):
                     n_cut += 1
                 elif tie:
                     n_tie_only += 1
+                    srt = st[order]
+                    a_, b_ = kk - 1, kk  # the chain of consecutive gaps < 2E around the cut (k2_select's run)
+                    while a_ > 0 and srt[a_ - 1] - srt[a_] < 2 * E:
+                        a_ -= 1
+                    while b_ + 1 < len(srt) and srt[b_] - srt[b_ + 1] < 2 * E:
+                        b_ += 1
+                    chains.append(b_ - a_ + 1)
                     hi, lo = st[order[kk - 1]], st[order[kk]]
                     band = np.flatnonzero((st >= lo - 2 * E) & (st <= hi + 2 * E))
                     bands.append(len(band))
@@ -69,4 +81,5 @@ for alpha in (0.90, 0.95, 0.98):
     print(f"alpha {alpha}: decisions {n_dec}, flagged by the cut {n_cut}, by the tie only {n_tie_only}; "
           f"tie band sizes {sorted(bands)[:5]}..{sorted(bands)[-5:] if bands else []} "
           f"(max {max(bands) if bands else 0}); band refinement reproduces the exact selection in "
-          f"{hybrid_ok}/{n_tie_only}", flush=True)
+          f"{hybrid_ok}/{n_tie_only}; k2_select runs: max {max(chains) if chains else 0}, "
+          f"> 16: {sum(c > 16 for c in chains)}, > 64: {sum(c > 64 for c in chains)}", flush=True)
