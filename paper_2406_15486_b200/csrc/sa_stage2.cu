@@ -73,10 +73,43 @@ __global__ void __launch_bounds__(kSelThreads)
       __syncthreads();
     }
   }
-  // sequential fp64 cumulative sum in sorted order (np.cumsum semantics): one
-  // thread, 32 scores loaded ahead per round so only the dependent adds are
-  // serial (adding the +0.0 tail leaves the sum bit-identical)
-  if (threadIdx.x == 0) {
+  if (eps > 0.0) {
+    // guard / certify passes: a parallel prefix sum (contiguous runs per
+    // thread, then a block scan of the run totals).  It differs from the
+    // sequential sum by ~1e-16 relative, far below the guard's margin E, and
+    // these passes keep a decision only when every margin exceeds E, so k and
+    // the picks are those of the sequential sum.
+    const int T = blockDim.x, per = (nb + T - 1) / T;
+    const int a0 = threadIdx.x * per, a1 = min(nb, a0 + per);
+    double run = 0.0;
+    for (int i = a0; i < a1; ++i) {
+      run += __longlong_as_double((long long)key[i]);
+      cum[i] = run;
+    }
+    double incl = run;  // inclusive scan of the run totals: warps, then warp totals
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    __shared__ double s_wsum[32];
+    if (lane == 31) s_wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      double v = lane < (T >> 5) ? s_wsum[lane] : 0.0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const double u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      s_wsum[lane] = v;
+    }
+    __syncthreads();
+    const double base = (incl - run) + (wid > 0 ? s_wsum[wid - 1] : 0.0);
+    for (int i = a0; i < a1; ++i) cum[i] += base;
+  } else if (threadIdx.x == 0) {
+    // the selection proper: sequential fp64 cumulative sum in sorted order
+    // (np.cumsum semantics), 32 scores loaded ahead per round so only the
+    // dependent adds are serial (adding the +0.0 tail leaves the sum bit-identical)
     double acc = 0.0;
     for (int i0 = 0; i0 < nb; i0 += 32) {
       double v[32];
