@@ -136,13 +136,22 @@ int sa_select(const double* col, const double* slash, int Hq, int chunk_n, int n
  * band recorded by sa_select whose pair is not flagged, the exact (fp64) mass
  * of every band block / bin over the pair's sampled rows is computed on the
  * FP64 tensor cores and normalised with stage 1's tensor-core row statistics
- * (left in the workspace by sa_stage1), and written over that block's col /
+ * (row_stats, see sa_workspace_offset), and written over that block's col /
  * slash score; band_pairs[hc] = 1 marks the refined pairs (for the certifying
  * sa_select).  bf16 path only. */
 int sa_band_table_len(int Hq, int chunk_n);
 int sa_refine_bands(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, int d, int blk, int group,
                     int q_head0, int chunk_n, int itv, const int* band, const int* flags, int* band_pairs,
-                    double* col, double* slash, void* workspace, size_t workspace_bytes, void* stream);
+                    const double* row_stats, double* col, double* slash, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+/* Byte offset of a workspace region of this geometry (< 0 on bad args).
+ * SA_WS_ROW_STATS: stage 1's per-sampled-row statistics, double
+ * [Hq*chunk_n*blk][2] (log2 max, sum) after a tensor-mode sa_stage1 -- copy
+ * them out to keep them for sa_refine_bands's row_stats, since later stage-1
+ * calls of the same geometry reuse the workspace. */
+#define SA_WS_ROW_STATS 0
+long long sa_workspace_offset(int S, int Hq, int Hkv, int d, int blk, int chunk_n, int dtype, int region);
 
 /* Stage 2b — replaces merge_index (filtering.py:198-230): extends every
  * chunk's picks over its query region, unions straddling blocks, forces the

@@ -19,6 +19,7 @@ SA_OK, SA_ERR_INVALID, SA_ERR_UNSUPPORTED, SA_ERR_INTERNAL, SA_ERR_CUDA = 0, -1,
 SA_BF16, SA_FP32 = 0, 1
 SA_STATUS_EMPTY_BLOCK, SA_STATUS_MASK, SA_STATUS_NORMALISER = 1, 2, 4
 SA_STAGE1_TENSOR, SA_STAGE1_EXACT = 0, 1
+SA_WS_ROW_STATS = 0
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -38,7 +39,8 @@ SIGNATURES = {
     "sa_stage1": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _Z, _P]),
     "sa_select": (_I, [_P, _P, _I, _I, _I, _D, _D, _D, _P, _D, _P, _P, _P, _P, _P, _P, _D, _P]),
     "sa_band_table_len": (_I, [_I, _I]),
-    "sa_refine_bands": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "sa_refine_bands": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "sa_workspace_offset": (ctypes.c_longlong, [_I, _I, _I, _I, _I, _I, _I, _I]),
     "sa_merge": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "sa_sampled_retained": (_I, [_I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _Z, _P, _P]),
     "sa_full_mask": (_I, [_I, _I, _P, _P, _P]),

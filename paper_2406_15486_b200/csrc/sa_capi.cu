@@ -250,18 +250,26 @@ int sa_band_table_len(int Hq, int chunk_n) {
   return Hq * chunk_n * 2 * kBandEntry;
 }
 
+long long sa_workspace_offset(int S, int Hq, int Hkv, int d, int blk, int chunk_n, int dtype, int region) {
+  if (S < 1 || Hq < 1 || Hkv < 1 || blk < 1 || chunk_n < 1) return fail(SA_ERR_INVALID, "sa_workspace_offset: bad args");
+  const Workspace L = workspace_layout(S, Hq, Hkv, d, blk, chunk_n, dtype);
+  if (region == SA_WS_ROW_STATS) return (long long)L.rowstat;
+  return fail(SA_ERR_INVALID, "sa_workspace_offset: unknown region");
+}
+
 int sa_refine_bands(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, int d, int blk, int group,
                     int q_head0, int chunk_n, int itv, const int* band, const int* flags, int* band_pairs,
-                    double* col, double* slash, void* workspace, size_t workspace_bytes, void* stream) {
+                    const double* row_stats, double* col, double* slash, void* workspace, size_t workspace_bytes,
+                    void* stream) {
   if (int e = check_geom(S, Hq, Hkv, d, blk, group, q_head0, dtype)) return e;
-  if (!q || !k || !band || !flags || !band_pairs || !col || !slash || !workspace)
+  if (!q || !k || !band || !flags || !band_pairs || !row_stats || !col || !slash || !workspace)
     return fail(SA_ERR_INVALID, "sa_refine_bands: null pointer");
   const Workspace L = workspace_layout(S, Hq, Hkv, d, blk, chunk_n, dtype);
   if (workspace_bytes < L.total) return fail(SA_ERR_INVALID, "sa_refine_bands: workspace too small");
   if (dtype != SA_BF16) return fail(SA_ERR_UNSUPPORTED, "sa_refine_bands: the band guard serves the bf16 path");
   Stage1Geom g{S, Hq, Hkv, d, blk, group, q_head0, chunk_n, itv, ceil_div(S, blk)};
-  return launch_refine_bands(g, q, k, dtype, band, flags, band_pairs, static_cast<char*>(workspace), L, col, slash,
-                             static_cast<cudaStream_t>(stream));
+  return launch_refine_bands(g, q, k, dtype, band, flags, band_pairs, row_stats, static_cast<char*>(workspace), L,
+                             col, slash, static_cast<cudaStream_t>(stream));
 }
 
 int sa_merge(const int* k_sel, const int* idx_sel, int Hq, int chunk_n, int nb, int S, int blk,

@@ -84,8 +84,8 @@ int launch_logit_bound(const Stage1Geom& g, const void* q, const void* k, char* 
 // each recorded band, normalised with the tensor-core row statistics, written
 // over those blocks' col / slash scores; marks band_pairs.
 int launch_refine_bands(const Stage1Geom& g, const void* q, const void* k, int dtype, const int* band,
-                        const int* flags, int* band_pairs, char* ws, const Workspace& L, double* col,
-                        double* slash, cudaStream_t st);
+                        const int* flags, int* band_pairs, const double* row_stats, char* ws, const Workspace& L,
+                        double* col, double* slash, cudaStream_t st);
 int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const int* only_flags,
                      char* ws, const Workspace& L, double* col, double* slash, cudaStream_t st);
 // rows' global max / sum, fold into part3, scatter into col / slash.  With

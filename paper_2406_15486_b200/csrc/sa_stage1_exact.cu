@@ -325,8 +325,8 @@ __global__ void k_band_scores(Stage1Geom g, const int* __restrict__ band, const 
 }  // namespace
 
 int launch_refine_bands(const Stage1Geom& g, const void* q, const void* k, int dtype, const int* band,
-                        const int* flags, int* band_pairs, char* ws, const Workspace& L, double* col,
-                        double* slash, cudaStream_t st) {
+                        const int* flags, int* band_pairs, const double* row_stats, char* ws, const Workspace& L,
+                        double* col, double* slash, cudaStream_t st) {
   int* items = reinterpret_cast<int*>(ws + L.band_items);
   const int n_ent = g.Hq * g.cn * 2;
   cudaMemsetAsync(items, 0, sizeof(int), st);
@@ -347,8 +347,7 @@ int launch_refine_bands(const Stage1Geom& g, const void* q, const void* k, int d
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k), g, items, pa, pb, pm);
   }
   if (int e = check_launch("band refinement: exact partials")) return e;
-  k_band_scores<<<n_ent, kRows, 0, st>>>(g, band, flags, pa, pb, pm,
-                                         reinterpret_cast<const double*>(ws + L.rowstat), col, slash);
+  k_band_scores<<<n_ent, kRows, 0, st>>>(g, band, flags, pa, pb, pm, row_stats, col, slash);
   return check_launch("band refinement: scores");
 }
 

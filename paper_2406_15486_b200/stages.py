@@ -157,6 +157,7 @@ class ReducedScores:
     slash: torch.Tensor
     mode: str
     logit_bound: torch.Tensor | None = None  # [H, cn] fp64 (tensor mode): the guard's error scale
+    row_stats: torch.Tensor | None = None    # [H*cn*blk*2] fp64 (tensor mode): sampled rows' (log2 max, sum)
 
     @property
     def chunks(self) -> tuple:
@@ -194,7 +195,13 @@ def block_reduce(samples: SampledScores, blk: int, mode: str | None = None) -> R
     slash = torch.empty_like(col)
     bound = torch.empty((b.Hq, plan.chunk_n), dtype=torch.float64, device=b.q.device) if mode == "tensor" else None
     _stage1(b, plan, col, slash, _lib.SA_STAGE1_TENSOR if mode == "tensor" else _lib.SA_STAGE1_EXACT, bound=bound)
-    return ReducedScores(b.S, blk, plan, b, col, slash, mode, bound)
+    row_stats = None
+    if mode == "tensor":  # the guard's band refinement needs them after later stage-1 calls reuse the workspace
+        off = int(_lib.load().sa_workspace_offset(b.S, b.Hq, b.Hkv, b.d, blk, plan.chunk_n, b.dtype_code,
+                                                   _lib.SA_WS_ROW_STATS))
+        rows = b.Hq * plan.chunk_n * blk
+        row_stats = _workspace(b, blk, plan.chunk_n)[off: off + rows * 16].view(torch.float64).clone()
+    return ReducedScores(b.S, blk, plan, b, col, slash, mode, bound, row_stats)
 
 
 # ---------------------------------------------------------------- stage 2
@@ -294,7 +301,7 @@ def select(reduced: ReducedScores, cfg: SparseConfig, guard: str = "auto",
         ws = _workspace(b, plan.blk, plan.chunk_n)
         dcall(dev, "sa_refine_bands", b.q.data_ptr(), b.k.data_ptr(), b.dtype_code, b.S, b.Hq, b.Hkv, b.d, plan.blk,
               b.group, b.q_head0, plan.chunk_n, plan.itv, band.data_ptr(), flags.data_ptr(), band_pairs.data_ptr(),
-              col, slash, ws.data_ptr(), ws.numel(), st)
+              reduced.row_stats.data_ptr(), col, slash, ws.data_ptr(), ws.numel(), st)
         dcall(dev, "sa_select", col, slash, H, cn, nb, cfg.alpha_c, cfg.alpha_s, guard_eps, bound.data_ptr(),
               GUARD_LOGIT_REF, flags.data_ptr(), band_pairs.data_ptr(), None, k_sel.data_ptr(), idx_sel.data_ptr(),
               band.data_ptr(), BAND_EPS, st)

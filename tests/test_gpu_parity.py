@@ -563,3 +563,34 @@ def test_host_path_shapes(sa, S, Hq, Hkv, cn, hpg):
     grid = np.concatenate([r.mask.to_dense() for r in res])
     assert np.array_equal(grid, r_dev.mask.to_dense())
     sa.release_staging()
+
+
+def test_band_refinement_survives_a_later_stage1(sa):
+    """The guard's band refinement normalises with stage 1's row statistics,
+    which later stage-1 calls of the same geometry overwrite in the shared
+    workspace (the tuner scores many tasks before selecting): they travel with
+    the ReducedScores, so selecting task A after scoring task B equals
+    selecting A right after scoring it -- and both equal the all-fp64 guard."""
+    from paper_2406_15486_b200 import synth
+    from paper_2406_15486_b200.config import SparseConfig, plan_chunks
+    S, Hq, Hkv, cn = 32768, 8, 2, 31
+    qa, ka, va, _ = synth.make_inputs(S, Hq, Hkv, 128, seed=21, device="cuda")
+    qb, kb, vb, _ = synth.make_inputs(S, Hq, Hkv, 128, seed=22, device="cuda")
+    cfg = SparseConfig(0.98, 0.98, chunk_n=cn)
+    plan = plan_chunks(S, cfg)
+    A, B = sa.HeadBatch.from_tensors(qa, ka, va), sa.HeadBatch.from_tensors(qb, kb, vb)
+    ra_fresh = sa.block_reduce(sa.sample_scores(A, plan), 128)
+    sel_fresh = sa.select(ra_fresh, cfg)
+    ra = sa.block_reduce(sa.sample_scores(A, plan), 128)
+    sa.block_reduce(sa.sample_scores(B, plan), 128)  # overwrites the workspace's row statistics
+    sel_late = sa.select(ra, cfg)
+    rx = sa.block_reduce(sa.sample_scores(A, plan), 128)
+    sel_exact = sa.select(rx, cfg, guard="always")
+    for s_ in (sel_fresh, sel_late):
+        assert torch.equal(s_.k_sel, sel_exact.k_sel)
+        for h in range(Hq):
+            for c in range(cn):
+                for d in range(2):
+                    k_ = int(s_.k_sel[h, c, d])
+                    assert torch.equal(s_.idx_sel[h, c, d, :k_], sel_exact.idx_sel[h, c, d, :k_])
+    assert sel_late.n_band_refined() + sel_late.n_rescored() > 0  # the guard had work to do
