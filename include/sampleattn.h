@@ -116,13 +116,14 @@ int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, i
  *     pair needs its exact re-score);
  *   - only the boundary tie within E: the blocks whose scores lie within 2E
  *     of the k-th largest are recorded in band (sa_band_table_len ints: per
- *     (hc, dir) [count, first rank, block / bin indices]) for
+ *     (hc, dir) [count, first rank, tie a, tie b, block / bin indices]) for
  *     sa_refine_bands -- or flags[hc] = 1 when band is NULL or they are more
  *     than 64.
  * Certify pass (band != NULL and only_flags != NULL, after sa_refine_bands):
  * k is recomputed on the refined scores and flags[hc] = 1 unless the alpha
  * cut clears E on both sides and the two blocks at the cut differ by more
- * than band_eps * (scale) * (s_a + s_b) (both refined) or E (otherwise).
+ * than band_eps * (scale) * (s_a + s_b) (both refined) or E (otherwise); two
+ * refined blocks closer than that are left to sa_certify_band_ties.
  * only_flags != NULL recomputes the flagged pairs only.  k_in != NULL
  * ([Hq][cn][2]) skips find_k and takes the given k (the reference's
  * arg_topk(scores, k), filtering.py:51-62). */
@@ -144,6 +145,20 @@ int sa_refine_bands(const void* q, const void* k, int dtype, int S, int Hq, int 
                     int q_head0, int chunk_n, int itv, const int* band, const int* flags, int* band_pairs,
                     const double* row_stats, double* col, double* slash, void* workspace, size_t workspace_bytes,
                     void* stream);
+
+/* Selection guard, band refinement, last step (after the certifying
+ * sa_select): when the two refined blocks a, b at a certified cut differ by no
+ * more than band_eps * scale * (s_a + s_b), the certify pass leaves them in the
+ * band entry and this call settles their order per row instead: row r's
+ * normaliser error scales both blocks' masses x_ra, x_rb alike, so the refined
+ * gap s_a - s_b is trusted when it exceeds band_eps * scale * sum_r |x_ra -
+ * x_rb| (scale = max(1, logit_bound[hc] / bound_ref)); else flags[hc] = 1 (the
+ * pair joins the exact re-score).  Reads the exact partials sa_refine_bands
+ * left in the workspace.  bf16 path only. */
+int sa_certify_band_ties(int dtype, int S, int Hq, int Hkv, int d, int blk, int chunk_n, int itv, const int* band,
+                         int* flags, const double* row_stats, const double* col, const double* slash,
+                         const double* logit_bound, double bound_ref, double band_eps, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* Byte offset of a workspace region of this geometry (< 0 on bad args).
  * SA_WS_ROW_STATS: stage 1's per-sampled-row statistics, double

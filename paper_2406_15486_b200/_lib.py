@@ -40,6 +40,7 @@ SIGNATURES = {
     "sa_select": (_I, [_P, _P, _I, _I, _I, _D, _D, _D, _P, _D, _P, _P, _P, _P, _P, _P, _D, _P]),
     "sa_band_table_len": (_I, [_I, _I]),
     "sa_refine_bands": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "sa_certify_band_ties": (_I, [_I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _D, _D, _P, _Z, _P]),
     "sa_workspace_offset": (ctypes.c_longlong, [_I, _I, _I, _I, _I, _I, _I, _I]),
     "sa_merge": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "sa_sampled_retained": (_I, [_I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _Z, _P, _P]),

@@ -272,6 +272,24 @@ int sa_refine_bands(const void* q, const void* k, int dtype, int S, int Hq, int 
                              col, slash, static_cast<cudaStream_t>(stream));
 }
 
+int sa_certify_band_ties(int dtype, int S, int Hq, int Hkv, int d, int blk, int chunk_n, int itv, const int* band,
+                         int* flags, const double* row_stats, const double* col, const double* slash,
+                         const double* logit_bound, double bound_ref, double band_eps, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  if (Hkv < 1) return fail(SA_ERR_INVALID, "sa_certify_band_ties: Hkv must be >= 1");
+  if (int e = check_geom(S, Hq, Hkv, d, blk, ceil_div(Hq, Hkv), 0, dtype)) return e;
+  if (!band || !flags || !row_stats || !col || !slash || !workspace)
+    return fail(SA_ERR_INVALID, "sa_certify_band_ties: null pointer");
+  if (chunk_n < 1 || itv < 1 || !(band_eps > 0.0) || (logit_bound && !(bound_ref > 0.0)))
+    return fail(SA_ERR_INVALID, "sa_certify_band_ties: bad chunk_n / itv / band_eps / bound_ref");
+  const Workspace L = workspace_layout(S, Hq, Hkv, d, blk, chunk_n, dtype);
+  if (workspace_bytes < L.total) return fail(SA_ERR_INVALID, "sa_certify_band_ties: workspace too small");
+  if (dtype != SA_BF16) return fail(SA_ERR_UNSUPPORTED, "sa_certify_band_ties: the band guard serves the bf16 path");
+  Stage1Geom g{S, Hq, Hkv, d, blk, 1, 0, chunk_n, itv, ceil_div(S, blk)};
+  return launch_band_ties(g, band, flags, row_stats, col, slash, logit_bound, bound_ref, band_eps,
+                          static_cast<char*>(workspace), L, static_cast<cudaStream_t>(stream));
+}
+
 int sa_merge(const int* k_sel, const int* idx_sel, int Hq, int chunk_n, int nb, int S, int blk,
              int itv, int sink_blocks, int local_blocks, int* kv_cnt, int* kv_idx,
              long long* active_blocks, long long* active_entries, void* stream) {

@@ -60,9 +60,12 @@ struct Workspace {
 Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int dtype);
 
 // Selection guard, band refinement: per (head, chunk, direction) the run of
-// nearly tied blocks at the cut -- [count, first rank, block / bin indices].
+// nearly tied blocks at the cut -- [count, first rank, tie a, tie b, block / bin
+// indices]; tie a / b: the two refined blocks at the certified cut whose order
+// the per-row test (k_band_ties) still has to settle, or -1.
 constexpr int kBandMax = 64;
-constexpr int kBandEntry = 2 + kBandMax;
+constexpr int kBandHdr = 4;
+constexpr int kBandEntry = kBandHdr + kBandMax;
 
 // key blocks one band entry can need: a slash bin reads two key blocks for each
 // of the (at most two) query blocks a sampled window spans
@@ -86,6 +89,11 @@ int launch_logit_bound(const Stage1Geom& g, const void* q, const void* k, char* 
 int launch_refine_bands(const Stage1Geom& g, const void* q, const void* k, int dtype, const int* band,
                         const int* flags, int* band_pairs, const double* row_stats, char* ws, const Workspace& L,
                         double* col, double* slash, cudaStream_t st);
+// Per-row certificate of the tie left at a certified band cut (band slots 2, 3);
+// flags the pair for the full re-score when it does not hold.
+int launch_band_ties(const Stage1Geom& g, const int* band, int* flags, const double* row_stats, const double* col,
+                     const double* slash, const double* bound, double bound_ref, double band_eps, char* ws,
+                     const Workspace& L, cudaStream_t st);
 int launch_stage1_tc(const Stage1Geom& g, const void* q, const void* k, const int* only_flags,
                      char* ws, const Workspace& L, double* col, double* slash, cudaStream_t st);
 // rows' global max / sum, fold into part3, scatter into col / slash.  With

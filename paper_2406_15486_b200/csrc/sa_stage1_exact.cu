@@ -96,21 +96,34 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
-// Work of one CTA: key blocks [kb0, kb1) of (head, chunk) hc.  The window's
+// Work of one CTA: the key blocks `kbs` of (head, chunk) hc.  The window's
 // query rows are staged once, raw (converted to fp64 per MMA fragment: one
 // conversion per 16 MMAs); K streams through two 64-dim fp64 smem slices, the
 // next slice's global loads issued into registers before the current slice's
 // MMAs so their latency hides under them.  Lane (gq = lane / 4, tg = lane % 4)
 // of warp w holds rows 8w + gq, keys 8nt + 2tg + {0, 1}.
-template <typename T>
+// The key blocks: a range (xf_pass: maxima run across the range, as the
+// fold expects) or entries of the band work list (xf_items: each block's
+// maximum its own, so a block listed twice is written with identical values).
+struct KbRange {
+  int kb0, n;
+  static constexpr bool kRunning = true;
+  __device__ __forceinline__ int operator()(int i) const { return kb0 + i; }
+};
+struct KbList {
+  const int* items;  // [count, (pair, key block)...]
+  int i0, n;
+  static constexpr bool kRunning = false;
+  __device__ __forceinline__ int operator()(int i) const { return items[2 + 2 * (i0 + i)]; }
+};
+
+template <typename T, typename KB>
 __device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __restrict__ k, const Stage1Geom& g,
-                                        int hc, int kb0, int kb1, double* __restrict__ pa,
-                                        double* __restrict__ pb, double* __restrict__ pm, T* qs,
-                                        double* ks) {
+                                        int hc, KB kbs, double* __restrict__ pa, double* __restrict__ pb,
+                                        double* __restrict__ pm, T* qs, double* ks) {
   const int h = hc / g.cn, c = hc - h * g.cn;
   const Win w = window_of(c, g.S, g.blk, g.itv);
-  kb1 = min(kb1, w.nkb);
-  if (kb0 >= kb1) return;
+  if (kbs.n <= 0) return;
   const int kvh = kv_head_of(h, g.group, g.q_head0);
   const int nr = w.se - w.ss, d = g.d, blk = g.blk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tg = lane & 3;
@@ -126,12 +139,16 @@ __device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __rest
   const int sr = threadIdx.x >> 2, sc = (threadIdx.x & 3) * 16;
   auto nk_of = [&](int kb) { return min(blk, w.se - kb * blk); };  // keys any sampled row can see
   Slice16<T> nxt;
-  nxt.load(kh + (size_t)kb0 * blk * d, sr, nk_of(kb0), sc, d);
+  int kb = kbs(0);
+  nxt.load(kh + (size_t)kb * blk * d, sr, nk_of(kb), sc, d);
   nxt.store(ks + sr * kPitchK + sc);
   __syncthreads();
   double m_run = -INFINITY;
   int buf = 0;
-  for (int kb = kb0; kb < kb1; ++kb) {
+  for (int it = 0; it < kbs.n; ++it) {
+    kb = kbs(it);
+    const int kb_next = it + 1 < kbs.n ? kbs(it + 1) : -1;
+    if (!KB::kRunning) m_run = -INFINITY;
     const int key0 = kb * blk;
     const int nk = nk_of(kb);
     double acc[16][2];
@@ -139,9 +156,9 @@ __device__ __forceinline__ void xf_work(const T* __restrict__ q, const T* __rest
     for (int nt = 0; nt < 16; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
     for (int ch = 0; ch < nch; ++ch) {
       // prefetch the next slice (this block's next 64 dims, or the next block's first)
-      const bool more = ch + 1 < nch || kb + 1 < kb1;
+      const bool more = ch + 1 < nch || kb_next >= 0;
       if (more) {
-        const int kbn = ch + 1 < nch ? kb : kb + 1, chn = ch + 1 < nch ? ch + 1 : 0;
+        const int kbn = ch + 1 < nch ? kb : kb_next, chn = ch + 1 < nch ? ch + 1 : 0;
         nxt.load(kh + (size_t)kbn * blk * d, sr, nk_of(kbn), chn * kDChunk + sc, d);
       }
       const double* kq = ks + buf * (kKeys * kPitchK);
@@ -215,12 +232,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kb0 = blockIdx.x * kb_per_cta;
   for (int f = blockIdx.y; f < n_pairs; f += gridDim.y) {  // uniform per CTA
     const int hc = list ? list[1 + f] : f;
-    xf_work(q, k, g, hc, kb0, kb0 + kb_per_cta, pa, pb, pm, qs, ks);
+    const int nkb = window_of(hc % g.cn, g.S, g.blk, g.itv).nkb;
+    xf_work(q, k, g, hc, KbRange{kb0, min(kb0 + kb_per_cta, nkb) - kb0}, pa, pb, pm, qs, ks);
     __syncthreads();  // qs / ks are reused by the next pair
   }
 }
 
-// Exact partials of an explicit (pair, key block) work list (band refinement).
+// Exact partials of an explicit (pair, key block) work list (band
+// refinement): CTA j takes the j-th run of ceil(n / gridDim.x) consecutive
+// items and stages Q once per stretch of one pair (k_band_items writes each
+// band entry's blocks contiguously, ascending).
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     xf_items(const T* __restrict__ q, const T* __restrict__ k, Stage1Geom g, const int* __restrict__ items,
@@ -229,96 +250,184 @@ __global__ void __launch_bounds__(kThreads, 1)
   T* qs = reinterpret_cast<T*>(smem_d);
   double* ks = reinterpret_cast<double*>(reinterpret_cast<char*>(smem_d) + kRows * kPitchQ * sizeof(T));
   const int n = items[0];
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {  // uniform per CTA
-    const int hc = items[1 + 2 * i], kb = items[2 + 2 * i];
-    xf_work(q, k, g, hc, kb, kb + 1, pa, pb, pm, qs, ks);
+  const int per = (n + gridDim.x - 1) / gridDim.x;
+  const int i1 = min(n, (int)(blockIdx.x + 1) * per);
+  for (int i = blockIdx.x * per; i < i1;) {  // uniform per CTA
+    const int hc = items[1 + 2 * i];
+    int j = i + 1;
+    while (j < i1 && items[1 + 2 * j] == hc) ++j;
+    xf_work(q, k, g, hc, KbList{items, i, j - i}, pa, pb, pm, qs, ks);
     __syncthreads();
+    i = j;
   }
 }
 
-// Band entry -> (pair, key block) work items: a col band lists key blocks, a
-// slash band lists offset bins o, each read from key blocks X - o (keys at or
+// Band entries -> (pair, key block) work items: a col band lists key blocks,
+// a slash band lists offset bins o, each read from key blocks X - o (keys at or
 // below the row's own offset in its block) and X - o - 1 for the query
-// block(s) X the sampled window spans.  Entries of pairs already flagged for
-// the full re-score are skipped.
-__global__ void k_band_items(Stage1Geom g, const int* __restrict__ band, const int* __restrict__ flags,
-                             int* __restrict__ band_pairs, int* __restrict__ items) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= g.Hq * g.cn * 2) return;
-  const int hc = e >> 1, dir = e & 1;
-  const int* ent = band + (size_t)e * kBandEntry;
-  const int n = ent[0];
-  if (n <= 0 || flags[hc]) return;
-  band_pairs[hc] = 1;
+// block(s) X the sampled window spans.  Pairs already flagged for the full
+// re-score are skipped.  One CTA per pair: the key blocks both of its entries
+// need are marked in a shared bitmap (dynamic smem, one bit per key block) and
+// written out once each, ascending, under one atomicAdd on the list's count.
+constexpr int kItemThreads = 128;
+
+__global__ void __launch_bounds__(kItemThreads)
+    k_band_items(Stage1Geom g, const int* __restrict__ band, const int* __restrict__ flags,
+                 int* __restrict__ band_pairs, int* __restrict__ items) {
+  extern __shared__ unsigned bits[];
+  __shared__ int s_warp[kItemThreads / 32], s_base;
+  const int hc = blockIdx.x;
+  const int* ent_c = band + (size_t)(2 * hc) * kBandEntry;
+  const int* ent_s = ent_c + kBandEntry;
+  const int nc = ent_c[0], ns = ent_s[0];
+  if ((nc <= 0 && ns <= 0) || flags[hc]) return;
+  if (threadIdx.x == 0) band_pairs[hc] = 1;
   const Win w = window_of(hc % g.cn, g.S, g.blk, g.itv);
   const int X0 = w.ss / g.blk, X1 = (w.se - 1) / g.blk;
-  int kbs[kBandItemsPerEntry];
-  int m = 0;
-  auto add = [&](int kb) {
-    if (kb < 0 || kb >= w.nkb) return;
-    for (int i = 0; i < m; ++i)
-      if (kbs[i] == kb) return;
-    kbs[m++] = kb;
+  const int nw = (w.nkb + 31) >> 5;
+  for (int i = threadIdx.x; i < nw; i += kItemThreads) bits[i] = 0u;
+  __syncthreads();
+  auto mark = [&](int kb) {
+    if (kb >= 0 && kb < w.nkb) atomicOr(bits + (kb >> 5), 1u << (kb & 31));
   };
-  for (int i = 0; i < n; ++i) {
-    const int b = ent[2 + i];
-    if (dir == 0) {
-      add(b);
-    } else {
-      for (int X = X0; X <= X1; ++X) {
-        add(X - b);
-        add(X - b - 1);
-      }
+  for (int i = threadIdx.x; i < nc; i += kItemThreads) mark(ent_c[kBandHdr + i]);
+  for (int i = threadIdx.x; i < ns; i += kItemThreads) {
+    const int b = ent_s[kBandHdr + i];
+    for (int X = X0; X <= X1; ++X) {
+      mark(X - b);
+      mark(X - b - 1);
     }
   }
-  const int at = atomicAdd(items, m);
-  for (int i = 0; i < m; ++i) {
-    items[1 + 2 * (at + i)] = hc;
-    items[2 + 2 * (at + i)] = kbs[i];
+  __syncthreads();
+  // thread t owns words [t * per, (t + 1) * per): count, block exclusive scan, write ascending
+  const int per = (nw + kItemThreads - 1) / kItemThreads;
+  const int w0 = threadIdx.x * per, w1 = min(nw, w0 + per);
+  int cnt = 0;
+  for (int i = w0; i < w1; ++i) cnt += __popc(bits[i]);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
   }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int i = 0; i < kItemThreads / 32; ++i) tot += s_warp[i];
+    s_base = atomicAdd(items, tot);
+  }
+  __syncthreads();
+  int at = s_base + incl - cnt;
+  for (int i = 0; i < wid; ++i) at += s_warp[i];
+  for (int i = w0; i < w1; ++i)
+    for (unsigned m = bits[i]; m; m &= m - 1) {
+      const int kb = (i << 5) + __ffs(m) - 1;
+      items[1 + 2 * at] = hc;
+      items[2 + 2 * at] = kb;
+      ++at;
+    }
 }
+
+// Row r's normalised exact mass in band block / bin b of pair hc: the exact
+// (fp64) partials of the key blocks it covers, scaled by the tensor-core row
+// statistics (M in log2 units, L): part_r * exp(m_r - M_r ln2) / L_r.
+struct BandRow {
+  const double *xa, *xb, *xm;
+  size_t row;  // (hc * blk + r) * nb: the row's partial-plane offset
+  int nkb, X;  // key blocks of the window; query block of the row
+  double M, invL;
+  __device__ double plane(const double* pl, int kb) const {
+    if (kb < 0 || kb >= nkb) return 0.0;
+    const double m = xm[row + kb];
+    return m == -INFINITY ? 0.0 : pl[row + kb] * exp(m - M) * invL;
+  }
+  __device__ double mass(int dir, int b) const {
+    if (dir == 0) {  // both parts of key block b share its maximum
+      if (b < 0 || b >= nkb) return 0.0;
+      const double m = xm[row + b];
+      return m == -INFINITY ? 0.0 : (xa[row + b] + xb[row + b]) * exp(m - M) * invL;
+    }
+    return plane(xa, X - b) + plane(xb, X - b - 1);
+  }
+};
+
+__device__ __forceinline__ BandRow band_row(const Stage1Geom& g, int hc, int r, const Win& w, const double* xa,
+                                            const double* xb, const double* xm, const double* rowstat) {
+  const size_t ro = (size_t)hc * g.blk + r;
+  return BandRow{xa, xb, xm, ro * g.nb, w.nkb, (w.ss + r) / g.blk, rowstat[ro * 2] * 0.6931471805599453,
+                 1.0 / rowstat[ro * 2 + 1]};
+}
+
+// Fixed-order sum over the window's rows of f(row) by one warp: lane l adds
+// rows l, l + 32, l + 64, l + 96 in that order, then a fixed xor-shuffle tree
+// (deterministic).  Returns the sum on every lane.
+template <typename F>
+__device__ __forceinline__ double warp_rows_sum(int nr, F f) {
+  double v[kRows / 32];
+#pragma unroll
+  for (int j = 0; j < kRows / 32; ++j) {  // unrolled: every row's loads in flight at once
+    const int r = (threadIdx.x & 31) + 32 * j;
+    v[j] = r < nr ? f(r) : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < kRows / 32; ++j) acc += v[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+constexpr int kBandWarps = 8;
 
 // Refined band scores: per band block, the sum over the window's rows of the
 // exact (fp64) mass in the block / bin, normalised with the tensor-core row
-// statistics (M in log2 units, L): s = sum_r part_r * exp(m_r - M_r ln2) / L_r.
-// Rows are added in a fixed order (deterministic).  Overwrites col / slash.
-__global__ void k_band_scores(Stage1Geom g, const int* __restrict__ band, const int* __restrict__ flags,
-                              const double* __restrict__ xa, const double* __restrict__ xb,
-                              const double* __restrict__ xm, const double* __restrict__ rowstat,
-                              double* __restrict__ col, double* __restrict__ slash) {
+// statistics.  One CTA per band entry, its warps stride over the entry's
+// blocks; rows are added in a fixed order (deterministic).  Overwrites col /
+// slash.
+__global__ void __launch_bounds__(kBandWarps * 32)
+    k_band_scores(Stage1Geom g, const int* __restrict__ band, const int* __restrict__ flags,
+                  const double* __restrict__ xa, const double* __restrict__ xb, const double* __restrict__ xm,
+                  const double* __restrict__ rowstat, double* __restrict__ col, double* __restrict__ slash) {
   const int e = blockIdx.x, hc = e >> 1, dir = e & 1;
   const int* ent = band + (size_t)e * kBandEntry;
   const int n = ent[0];
   if (n <= 0 || flags[hc]) return;
-  __shared__ double part[kRows];
   const Win w = window_of(hc % g.cn, g.S, g.blk, g.itv);
-  const int nr = w.se - w.ss, r = threadIdx.x;
-  double M = 0.0, invL = 0.0;
-  int X = 0;
-  if (r < nr) {
-    const size_t ro = (size_t)hc * g.blk + r;
-    M = rowstat[ro * 2] * 0.6931471805599453;
-    invL = 1.0 / rowstat[ro * 2 + 1];
-    X = (w.ss + r) / g.blk;
+  const int nr = w.se - w.ss;
+  double* out = (dir == 0 ? col : slash) + (size_t)hc * g.nb;
+  for (int i = threadIdx.x >> 5; i < n; i += kBandWarps) {
+    const int b = ent[kBandHdr + i];
+    const double acc = warp_rows_sum(nr, [&](int r) { return band_row(g, hc, r, w, xa, xb, xm, rowstat).mass(dir, b); });
+    if ((threadIdx.x & 31) == 0) out[b] = acc;
   }
-  auto plane = [&](const double* pl, int kb) -> double {  // exact part of (row r, key block kb), normalised
-    if (kb < 0 || kb >= w.nkb) return 0.0;
-    const size_t o = ((size_t)hc * g.blk + r) * g.nb + kb;
-    const double m = xm[o];
-    return m == -INFINITY ? 0.0 : pl[o] * exp(m - M) * invL;
-  };
-  for (int i = 0; i < n; ++i) {
-    const int b = ent[2 + i];
-    double v = 0.0;
-    if (r < nr) v = dir == 0 ? plane(xa, b) + plane(xb, b) : plane(xa, X - b) + plane(xb, X - b - 1);
-    part[r] = v;
-    __syncthreads();
-    if (r == 0) {
-      double acc = 0.0;
-      for (int t = 0; t < nr; ++t) acc += part[t];
-      (dir == 0 ? col : slash)[(size_t)hc * g.nb + b] = acc;
-    }
-    __syncthreads();
+}
+
+// Per-row certificate of the order of the two refined blocks a, b at a
+// certified cut (band entry slots 2, 3, left by sa_select's certify pass when
+// band_eps * (s_a + s_b) could not settle it).  Row r's normaliser error d_r
+// (|d_r| <= band_eps * scale) scales x_ra and x_rb alike, so the refined
+// difference s_a - s_b = sum_r (x_ra - x_rb) / (1 + d_r) is off by at most
+// band_eps * scale * sum_r |x_ra - x_rb|: a larger gap fixes the exact order;
+// else the pair is flagged for the full re-score.
+__global__ void k_band_ties(Stage1Geom g, const int* __restrict__ band, int* __restrict__ flags,
+                            const double* __restrict__ xa, const double* __restrict__ xb,
+                            const double* __restrict__ xm, const double* __restrict__ rowstat,
+                            const double* __restrict__ col, const double* __restrict__ slash,
+                            const double* __restrict__ bound, double bound_ref, double band_eps) {
+  const int e = blockIdx.x, hc = e >> 1, dir = e & 1;
+  const int* ent = band + (size_t)e * kBandEntry;
+  if (ent[0] <= 0 || ent[2] < 0 || flags[hc]) return;
+  const int a = ent[2], b = ent[3];
+  const Win w = window_of(hc % g.cn, g.S, g.blk, g.itv);
+  const double W = warp_rows_sum(w.se - w.ss, [&](int r) {
+    const BandRow br = band_row(g, hc, r, w, xa, xb, xm, rowstat);
+    return fabs(br.mass(dir, a) - br.mass(dir, b));
+  });
+  if (threadIdx.x == 0) {
+    const double* s = (dir == 0 ? col : slash) + (size_t)hc * g.nb;
+    const double scale = bound ? fmax(1.0, bound[hc] / bound_ref) : 1.0;
+    if (!(s[a] - s[b] > band_eps * scale * W)) atomicOr(flags + hc, 1);
   }
 }
 
@@ -331,7 +440,9 @@ int launch_refine_bands(const Stage1Geom& g, const void* q, const void* k, int d
   const int n_ent = g.Hq * g.cn * 2;
   cudaMemsetAsync(items, 0, sizeof(int), st);
   cudaMemsetAsync(band_pairs, 0, sizeof(int) * g.Hq * g.cn, st);
-  k_band_items<<<ceil_div(n_ent, 128), 128, 0, st>>>(g, band, flags, band_pairs, items);
+  const int bitmap_bytes = ceil_div(g.nb, 32) * 4;
+  if (bitmap_bytes > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(&k_band_items), bitmap_bytes);
+  k_band_items<<<g.Hq * g.cn, kItemThreads, bitmap_bytes, st>>>(g, band, flags, band_pairs, items);
   if (int e = check_launch("band refinement: work list")) return e;
   const size_t plane = (size_t)g.Hq * g.cn * g.blk * g.nb;
   double* pa = reinterpret_cast<double*>(ws + L.x_part);
@@ -339,16 +450,26 @@ int launch_refine_bands(const Stage1Geom& g, const void* q, const void* k, int d
   double* pm = pb + plane;
   if (dtype == SA_FP32) {
     set_smem_attr(reinterpret_cast<const void*>(&xf_items<float>), xf_smem_bytes<float>());
-    xf_items<float><<<2 * 148, kThreads, xf_smem_bytes<float>(), st>>>(
+    xf_items<float><<<148, kThreads, xf_smem_bytes<float>(), st>>>(
         static_cast<const float*>(q), static_cast<const float*>(k), g, items, pa, pb, pm);
   } else {
     set_smem_attr(reinterpret_cast<const void*>(&xf_items<__nv_bfloat16>), xf_smem_bytes<__nv_bfloat16>());
-    xf_items<__nv_bfloat16><<<2 * 148, kThreads, xf_smem_bytes<__nv_bfloat16>(), st>>>(
+    xf_items<__nv_bfloat16><<<148, kThreads, xf_smem_bytes<__nv_bfloat16>(), st>>>(
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k), g, items, pa, pb, pm);
   }
   if (int e = check_launch("band refinement: exact partials")) return e;
-  k_band_scores<<<n_ent, kRows, 0, st>>>(g, band, flags, pa, pb, pm, row_stats, col, slash);
+  k_band_scores<<<n_ent, kBandWarps * 32, 0, st>>>(g, band, flags, pa, pb, pm, row_stats, col, slash);
   return check_launch("band refinement: scores");
+}
+
+int launch_band_ties(const Stage1Geom& g, const int* band, int* flags, const double* row_stats, const double* col,
+                     const double* slash, const double* bound, double bound_ref, double band_eps, char* ws,
+                     const Workspace& L, cudaStream_t st) {
+  const size_t plane = (size_t)g.Hq * g.cn * g.blk * g.nb;
+  const double* pa = reinterpret_cast<const double*>(ws + L.x_part);
+  k_band_ties<<<g.Hq * g.cn * 2, 32, 0, st>>>(g, band, flags, pa, pa + plane, pa + 2 * plane, row_stats, col,
+                                                 slash, bound, bound_ref, band_eps);
+  return check_launch("band refinement: per-row tie certificate");
 }
 
 // Per sampled row: global max M and normaliser L over the row's key blocks.

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kSelThreads)
     int* ent = band ? band + ((size_t)hc * 2 + dir) * kBandEntry : nullptr;
     const bool certify = band && only;  // re-select of refined pairs
     const double E = eps * total * scale_b;  // error bound of tensor-core scores (guard)
-    if (ent && !certify) ent[0] = 0;
+    if (ent && !certify) ent[0] = 0, ent[2] = ent[3] = -1;
     if (eps > 0.0 && k > 0 && flags && !k_in && !certify) {
       // guard pass: margin widened for large-logit pairs (bound: see k_pair_bound, sa_stage1_tc.cu)
       const double m1 = cum[k - 1] - target, m2 = k >= 2 ? target - cum[k - 2] : INFINITY;
@@ -167,25 +167,33 @@ __global__ void __launch_bounds__(kSelThreads)
         } else {
           ent[0] = z - a + 1;
           ent[1] = a;
-          for (int i = a; i <= z; ++i) ent[2 + i - a] = idx[i];
+          for (int i = a; i <= z; ++i) ent[kBandHdr + i - a] = idx[i];
         }
       }
     } else if (certify && eps > 0.0 && k > 0 && flags && ent) {
       // certify a refined pair: band blocks now carry near-exact scores, the
       // others tensor-core ones (error <= E, which also bounds the prefix
       // sums), so k must clear the alpha cut by E on both sides, and the two
-      // blocks at the cut must differ by more than their own error: the
-      // refinement's band_eps * (s_a + s_b) when both are refined, E otherwise
+      // blocks at the cut must differ by more than their own error: E unless
+      // both are refined; for two refined blocks band_eps * (s_a + s_b)
+      // settles it here, and a closer pair is left to k_band_ties' per-row
+      // bound (band_eps * sum_r |x_ra - x_rb| <= band_eps * (s_a + s_b))
       const double m1 = cum[k - 1] - target, m2 = k >= 2 ? target - cum[k - 2] : INFINITY;
       bool ok = m1 >= E && m2 >= E;
+      ent[2] = ent[3] = -1;
       if (ok && k < nb) {
         const double sa = sc(k - 1), sb = sc(k);
         bool ra = false, rb = false;
         for (int i = 0; i < ent[0]; ++i) {
-          ra |= ent[2 + i] == idx[k - 1];
-          rb |= ent[2 + i] == idx[k];
+          ra |= ent[kBandHdr + i] == idx[k - 1];
+          rb |= ent[kBandHdr + i] == idx[k];
         }
-        ok = (ra && rb) ? sa - sb > band_eps * scale_b * (sa + sb) : sa - sb >= E;
+        if (!(ra && rb)) {
+          ok = sa - sb >= E;
+        } else if (!(sa - sb > band_eps * scale_b * (sa + sb))) {
+          ent[2] = idx[k - 1];
+          ent[3] = idx[k];
+        }
       }
       if (!ok) atomicOr(flags + hc, 1);
     }

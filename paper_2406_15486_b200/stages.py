@@ -305,6 +305,9 @@ def select(reduced: ReducedScores, cfg: SparseConfig, guard: str = "auto",
         dcall(dev, "sa_select", col, slash, H, cn, nb, cfg.alpha_c, cfg.alpha_s, guard_eps, bound.data_ptr(),
               GUARD_LOGIT_REF, flags.data_ptr(), band_pairs.data_ptr(), None, k_sel.data_ptr(), idx_sel.data_ptr(),
               band.data_ptr(), BAND_EPS, st)
+        dcall(dev, "sa_certify_band_ties", b.dtype_code, b.S, b.Hq, b.Hkv, b.d, plan.blk, plan.chunk_n, plan.itv,
+              band.data_ptr(), flags.data_ptr(), reduced.row_stats.data_ptr(), col, slash, bound.data_ptr(),
+              GUARD_LOGIT_REF, BAND_EPS, ws.data_ptr(), ws.numel(), st)
         # everything else the guard flagged: the exact (fp64) stage 1 of the pair, then a fresh selection
         _stage1(b, plan, reduced.col, reduced.slash, _lib.SA_STAGE1_EXACT, only=flags)
         dcall(dev, "sa_select", col, slash, H, cn, nb, cfg.alpha_c, cfg.alpha_s, 0.0, None, 1.0, None,

@@ -171,23 +171,31 @@ def test_selection_matches_oracle_at_1m(sa):
         assert tuple(int(x) for x in res.mask.head(0).active_for(qb)) == tuple(sorted(want)), qb
 
 
-@pytest.mark.parametrize("config", ["c3", "c4_77"])
+@pytest.mark.parametrize("config", ["c3", "c4_77", "c2ref"])
 def test_guard_auto_equals_all_fp64_on_every_head(sa, config):
     """Certifies the selection guard on the full benchmark workloads: with
     guard="auto" (tensor-core scores, fp64 re-score of the flagged pairs only)
     every head's selected index sets and merged mask equal those of
     guard="always" (every pair scored in fp64, the reference's arithmetic) --
     C3 at alpha 0.90 / 0.95 / 0.98 (32 heads) and C4 at 10 % sampling
-    (32 heads x 77 chunks).  A decision the tensor-core error could flip that
-    the margin test missed would show up here."""
+    (32 heads x 77 chunks), and the C2 shape on the reference's calibrated
+    heads (bench --config c2ref: density 0.97, nearly every decision a tie that
+    the band refinement and its per-row certificate settle).  A decision the
+    tensor-core error could flip that the margin test missed would show up here."""
     import torch
 
-    from paper_2406_15486_b200 import synth
+    from paper_2406_15486_b200 import refsynth, synth
     if config == "c3":
         S, Hq, Hkv, cn, alphas = 131072, 32, 2, 1, (0.90, 0.95, 0.98)
-    else:
+    elif config == "c4_77":
         S, Hq, Hkv, cn, alphas = 98304, 32, 8, 77, (0.95,)
-    q, k, v, _ = synth.make_inputs(S, Hq, Hkv, seed=0, device="cuda")
+    else:
+        S, Hq, Hkv, cn, alphas = 32768, 32, 2, 1, (0.90, 0.95, 0.98)
+    if config == "c2ref":  # bench.py's REF_SINKS / REF_SLASHES
+        spec = refsynth.SyntheticSpec(S, 128, Hkv, ((0, 0.18), (1500, 0.14)), ((0, 0.60),), 1.0, 0)
+        q, k, v, _ = refsynth.calibrated_gqa_inputs(spec, Hq, Hkv, dtype=torch.bfloat16, device="cuda")
+    else:
+        q, k, v, _ = synth.make_inputs(S, Hq, Hkv, seed=0, device="cuda")
     for alpha in alphas:
         _, ra = sa.sample_attention(q, k, v, alpha=alpha, chunk_n=cn, guard="auto")
         _, rw = sa.sample_attention(q, k, v, alpha=alpha, chunk_n=cn, guard="always")
