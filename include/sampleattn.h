@@ -118,7 +118,7 @@ int sa_stage1(const void* q, const void* k, int dtype, int S, int Hq, int Hkv, i
  *     of the k-th largest are recorded in band (sa_band_table_len ints: per
  *     (hc, dir) [count, first rank, tie a, tie b, block / bin indices]) for
  *     sa_refine_bands -- or flags[hc] = 1 when band is NULL or they are more
- *     than 64.
+ *     than 512.
  * Certify pass (band != NULL and only_flags != NULL, after sa_refine_bands):
  * k is recomputed on the refined scores and flags[hc] = 1 unless the alpha
  * cut clears E on both sides and the two blocks at the cut differ by more

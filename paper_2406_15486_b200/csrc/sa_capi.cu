@@ -132,7 +132,7 @@ Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int d
   L.kmax2 = off;
   off = align_up(off + (size_t)Hkv * sizeof(unsigned));
   L.band_items = off;
-  off = align_up(off + (1 + 2 * (size_t)Hq * cn * 2 * kBandItemsPerEntry) * sizeof(int));
+  off = align_up(off + (1 + 2 * (size_t)Hq * cn * nb) * sizeof(int));  // each pair's key blocks at most once
   L.total = off;
   return L;
 }

@@ -63,13 +63,12 @@ Workspace workspace_layout(int S, int Hq, int Hkv, int d, int blk, int cn, int d
 // nearly tied blocks at the cut -- [count, first rank, tie a, tie b, block / bin
 // indices]; tie a / b: the two refined blocks at the certified cut whose order
 // the per-row test (k_band_ties) still has to settle, or -1.
-constexpr int kBandMax = 64;
+// Bands of up to 512 blocks are refined (the reference's calibrated heads
+// reach ~350 at 128K, where the refinement still touches about half the key
+// blocks a full re-score does); a wider band sends the pair to the re-score.
+constexpr int kBandMax = 512;
 constexpr int kBandHdr = 4;
 constexpr int kBandEntry = kBandHdr + kBandMax;
-
-// key blocks one band entry can need: a slash bin reads two key blocks for each
-// of the (at most two) query blocks a sampled window spans
-constexpr int kBandItemsPerEntry = 4 * kBandMax;
 
 // Launchers (return SA_OK or an error code; all stream-ordered).
 int launch_stage1_exact(const Stage1Geom& g, const void* q, const void* k, int dtype,
