@@ -109,6 +109,16 @@ def test_c_abi_rejects_bad_arguments_without_touching_the_gpu():
     assert lib.sa_select(fake, fake, 1, 1, 8, 0.9, 0.9, 1e-7, fake, 0.0, fake, None, None, fake, fake, None, 0.0, None) \
         == _lib.SA_ERR_INVALID and "bound_ref" in _err(lib)
     assert lib.sa_merge(fake, fake, 1, 1, 7, 1024, 128, 1024, 0, 1, fake, fake, None, None, None) == _lib.SA_ERR_INVALID
+    # band guard: the per-row tie certificate checks its pointers, eps and workspace before any launch
+    ws_bytes = lib.sa_workspace_bytes(4096, 2, 1, 128, 128, 1, _lib.SA_BF16)
+    assert lib.sa_certify_band_ties(_lib.SA_BF16, 4096, 2, 1, 128, 128, 1, 4096, None, fake, fake, fake, fake, None,
+                                    320.0, 3e-5, fake, ws_bytes, None) == _lib.SA_ERR_INVALID and "null" in _err(lib)
+    assert lib.sa_certify_band_ties(_lib.SA_BF16, 4096, 2, 1, 128, 128, 1, 4096, fake, fake, fake, fake, fake, None,
+                                    320.0, 0.0, fake, ws_bytes, None) == _lib.SA_ERR_INVALID and "band_eps" in _err(lib)
+    assert lib.sa_certify_band_ties(_lib.SA_BF16, 4096, 2, 1, 128, 128, 1, 4096, fake, fake, fake, fake, fake, None,
+                                    320.0, 3e-5, fake, 16, None) == _lib.SA_ERR_INVALID and "workspace" in _err(lib)
+    assert lib.sa_certify_band_ties(_lib.SA_FP32, 4096, 2, 1, 128, 128, 1, 4096, fake, fake, fake, fake, fake, None,
+                                    320.0, 3e-5, fake, 1 << 30, None) == _lib.SA_ERR_UNSUPPORTED
     assert lib.sa_schedule_len(0, 8, 1, 0) < 0
     assert lib.sa_schedule_len(32, 1024, 16, 0) == 2 * 32 * 1024 // 2
     assert lib.sa_schedule_len(3, 5, 3, 0) == 2 * (5 + 3)  # one head pair + the odd head's adjacent-block pairs
