@@ -42,18 +42,26 @@ if "reference" in sys.argv and "--impl" in sys.argv:
     os.environ["OPENBLAS_NUM_THREADS"] = os.environ["OMP_NUM_THREADS"] = _cores
 
 CONFIGS = {
-    # name: (S, Hq, Hkv, alpha, chunk_n, description)
-    "c3": (131072, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 128K, bf16, alpha 0.95, chunk_n 1"),
-    "c2": (32768, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 32K, bf16, alpha 0.95, chunk_n 1"),
-    "c4": (98304, 32, 8, 0.95, 15, "InternLM2-7B attention shape, seq 96K, bf16, alpha 0.95, 2% sampling"),
-    "c5": (1048576, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 1M, bf16, alpha 0.95, heads sharded + NVLink gather"),
+    # name: (S, Hq, Hkv, alpha, chunk_n, description of the shape; alpha and sampling are appended from the run's values)
+    "c3": (131072, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 128K, bf16"),
+    "c2": (32768, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 32K, bf16"),
+    "c4": (98304, 32, 8, 0.95, 15, "InternLM2-7B attention shape, seq 96K, bf16"),
+    "c5": (1048576, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 1M, bf16, heads sharded + NVLink gather"),
     # the same shapes on heads from the reference's OWN calibrated generator (refsynth: SURVEY.md's C1 family of
     # planted structures, one calibrated head per KV group, q heads redraw their noise dims)
-    "c2ref": (32768, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 32K, bf16, alpha 0.95, chunk_n 1, "
-                                     "reference-calibrated heads"),
-    "c3ref": (131072, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 128K, bf16, alpha 0.95, chunk_n 1, "
-                                      "reference-calibrated heads"),
+    "c2ref": (32768, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 32K, bf16, reference-calibrated heads"),
+    "c3ref": (131072, 32, 2, 0.95, 1, "ChatGLM3-6B attention shape, seq 128K, bf16, reference-calibrated heads"),
 }
+
+
+def describe(desc: str, S: int, alpha: float, chunk_n: int) -> str:
+    """The workload string with the alpha and sampling actually run (chunk_n sampled
+    128-row windows = chunk_n*128/S of the queries, ref sampler.py:88-118)."""
+    pct = 100.0 * chunk_n * 128 / S
+    samp = f"chunk_n {chunk_n}" if chunk_n == 1 else f"{pct:.0f}% sampling (chunk_n {chunk_n})"
+    return f"{desc}, alpha {alpha:g}, {samp}"
+
+
 # planted structures of the *ref configs (SURVEY.md section 8d, C1 family: sinks at 0 and 1500, local window)
 REF_SINKS = ((0, 0.18), (1500, 0.14))
 REF_SLASHES = ((0, 0.60),)
@@ -247,7 +255,7 @@ def main():
         chunk_n = args.chunk_n
     gather = args.gather or args.config == "c5"
     d = 128
-    workload = {"workload": desc, "S": S, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d, "alpha": alpha,
+    workload = {"workload": describe(desc, S, alpha, chunk_n), "S": S, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d, "alpha": alpha,
                 "chunk_n": chunk_n, "blk": 128, "parallelism": f"heads/{world}" + ("+gather" if gather else ""),
                 "l2": "flushed between steps"}
 
