@@ -239,7 +239,7 @@ def main():
     ap.add_argument("--guard", default="auto", choices=["auto", "always", "never"])
     ap.add_argument("--chunk-n", type=int, default=None)
     ap.add_argument("--no-graph", action="store_true", help="launch the stages from Python instead of CUDA graphs")
-    ap.add_argument("--gather", action="store_true", help="all-gather outputs over NCCL (default for c5)")
+    ap.add_argument("--gather", action="store_true", help="gather every rank's outputs to every rank (fused into stage 3 over NVLink peer memory; default for c5)")
     ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if not args.dry_run else args.warmup
@@ -301,6 +301,8 @@ def main():
         def n_rescored(self):
             return 0
 
+    # the job's [Hq, S, d] output on every rank (the p2p gather maps the peers' copies once)
+    gather_buf = torch.empty((Hq, S, d), dtype=q.dtype, device=dev) if (gather and world > 1) else None
     use_graph = not (gather and world > 1) and not args.no_graph
     gexec = None
     if use_graph:  # the serving path: the three stages captured as CUDA graphs on static buffers
@@ -336,7 +338,7 @@ def main():
                 return o_, r_
 
             sample_attention_sharded(q, k, v, shard, heads_per_chunk=1, compute_fn=fn, alpha=alpha,
-                                     chunk_n=chunk_n, guard=args.guard)
+                                     chunk_n=chunk_n, guard=args.guard, out=gather_buf)
             return out, _Res(masks)
         return sa.sample_attention(q, k, v, alpha=alpha, chunk_n=chunk_n, guard=args.guard, timings=timings,
                                    q_head0=q_head0, group=group, out=out)

@@ -222,6 +222,31 @@ int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, in
                       const int* kv_idx, const int* order, void* out, float* lse,
                       long long* touched, void* stream);
 
+/* Stage 3 with the output gather fused into its epilogue (the 1M-token
+ * configuration, heads sharded over GPUs; replaces sa_sparse_forward followed
+ * by an all-gather of the per-rank outputs, ref pipeline.py:169-176 loops the
+ * heads of one process).  Same arguments and result as sa_sparse_forward
+ * (bf16 only); in addition every output row is stored, as soon as its tile
+ * finishes, into the n_peer buffers peer_out[0..n_peer) -- device pointers
+ * (peer-mapped through sa_ipc_open) to the same [Hq][S][d] rows of the other
+ * ranks' gather buffers -- so the NVLink transfer overlaps the attention tile
+ * by tile.  peer_out is a HOST array; n_peer <= SA_MAX_PEERS.  Completion on a
+ * peer is the caller's to signal (stream sync + barrier). */
+#define SA_MAX_PEERS 7
+int sa_sparse_forward_peers(const void* q, const void* k, const void* v, int dtype, int S, int Hq,
+                            int Hkv, int d, int blk, int group, int q_head0, const int* kv_cnt,
+                            const int* kv_idx, const int* order, void* out, float* lse,
+                            long long* touched, void* const* peer_out, int n_peer, void* stream);
+
+/* CUDA IPC of a gather buffer between the ranks of one node.  sa_ipc_export
+ * writes the 64-byte handle of the allocation holding ptr and ptr's byte
+ * offset inside it; a peer process passes both to sa_ipc_open, adds the
+ * offset to the returned base, and closes the base with sa_ipc_close. */
+#define SA_IPC_HANDLE_BYTES 64
+int sa_ipc_export(const void* ptr, void* handle, unsigned long long* offset);
+int sa_ipc_open(const void* handle, void** base);
+int sa_ipc_close(void* base);
+
 #ifdef __cplusplus
 }
 #endif

@@ -48,7 +48,14 @@ SIGNATURES = {
     "sa_schedule_len": (_I, [_I, _I, _I, _I]),
     "sa_schedule": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P]),
     "sa_sparse_forward": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "sa_sparse_forward_peers": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P,
+                                     ctypes.POINTER(_P), _I, _P]),
+    "sa_ipc_export": (_I, [_P, _P, ctypes.POINTER(ctypes.c_ulonglong)]),
+    "sa_ipc_open": (_I, [_P, ctypes.POINTER(_P)]),
+    "sa_ipc_close": (_I, [_P]),
 }
+SA_MAX_PEERS = 7
+SA_IPC_HANDLE_BYTES = 64
 
 _lib = None
 _load_error = None

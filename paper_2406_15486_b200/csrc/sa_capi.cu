@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -49,6 +50,21 @@ EncodeTiledFn encode_fn() {
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+// cuMemGetAddressRange (driver API through the runtime's entry-point query, so
+// the library needs no -lcuda): the allocation base a CUDA IPC handle refers to
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+AddrRangeFn addr_range_fn() {
+  static AddrRangeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<AddrRangeFn>(p);
   });
   return fn;
 }
@@ -350,6 +366,52 @@ int sa_sparse_forward(const void* q, const void* k, const void* v, int dtype, in
   return launch_sparse_simt(static_cast<const float*>(q), static_cast<const float*>(k),
                             static_cast<const float*>(v), S, Hq, Hkv, d, blk, group, q_head0, kv_cnt,
                             kv_idx, order, n_order, static_cast<float*>(out), lse, touched, st);
+}
+
+int sa_sparse_forward_peers(const void* q, const void* k, const void* v, int dtype, int S, int Hq, int Hkv,
+                            int d, int blk, int group, int q_head0, const int* kv_cnt, const int* kv_idx,
+                            const int* order, void* out, float* lse, long long* touched, void* const* peer_out,
+                            int n_peer, void* stream) {
+  if (int e = check_geom(S, Hq, Hkv, d, blk, group, q_head0, dtype)) return e;
+  if (!q || !k || !v || !kv_cnt || !kv_idx || !out)
+    return fail(SA_ERR_INVALID, "sa_sparse_forward_peers: null pointer");
+  if (n_peer < 0 || n_peer > SA_MAX_PEERS || (n_peer > 0 && !peer_out))
+    return fail(SA_ERR_INVALID, "sa_sparse_forward_peers: n_peer must be in [0, SA_MAX_PEERS] with peer_out set");
+  for (int p = 0; p < n_peer; ++p)
+    if (!peer_out[p]) return fail(SA_ERR_INVALID, "sa_sparse_forward_peers: null peer buffer");
+  if (dtype != SA_BF16) return fail(SA_ERR_UNSUPPORTED, "sa_sparse_forward_peers: bf16 only");
+  return launch_sparse_share(q, k, v, S, Hq, Hkv, group, q_head0, kv_cnt, kv_idx, order, out, lse, touched,
+                             static_cast<cudaStream_t>(stream), peer_out, n_peer);
+}
+
+int sa_ipc_export(const void* ptr, void* handle, unsigned long long* offset) {
+  if (!ptr || !handle || !offset) return fail(SA_ERR_INVALID, "sa_ipc_export: null pointer");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (!addr_range_fn() || addr_range_fn()(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return fail(SA_ERR_CUDA, "sa_ipc_export: cuMemGetAddressRange failed (not a device allocation?)");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return fail(SA_ERR_CUDA, std::string("sa_ipc_export: ") + cudaGetErrorString(e));
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = reinterpret_cast<CUdeviceptr>(ptr) - base;
+  return SA_OK;
+}
+
+int sa_ipc_open(const void* handle, void** base) {
+  if (!handle || !base) return fail(SA_ERR_INVALID, "sa_ipc_open: null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(SA_ERR_CUDA, std::string("sa_ipc_open: ") + cudaGetErrorString(e));
+  return SA_OK;
+}
+
+int sa_ipc_close(void* base) {
+  if (!base) return fail(SA_ERR_INVALID, "sa_ipc_close: null pointer");
+  cudaError_t e = cudaIpcCloseMemHandle(base);
+  if (e != cudaSuccess) return fail(SA_ERR_CUDA, std::string("sa_ipc_close: ") + cudaGetErrorString(e));
+  return SA_OK;
 }
 
 }  // extern "C"

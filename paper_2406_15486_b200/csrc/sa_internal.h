@@ -162,6 +162,7 @@ __host__ __device__ inline int n_units(int Hq, int nb, int group, int q_head0) {
 
 int launch_sparse_share(const void* q, const void* k, const void* v, int S, int Hq, int Hkv, int group,
                         int q_head0, const int* kv_cnt, const int* kv_idx, const int* units, void* out,
-                        float* lse, long long* touched, cudaStream_t st);
+                        float* lse, long long* touched, cudaStream_t st, void* const* peer_out = nullptr,
+                        int n_peer = 0);
 
 }  // namespace sa

@@ -37,6 +37,14 @@ struct K3TileBars {
   uint64_t* o_full;   // last PV done                  (tcgen05.commit)
 };
 
+// Output rows also stored into up to kMax peer gather buffers (peer-mapped
+// device pointers at the same [Hq][S][d] rows), tile by tile over NVLink.
+struct K3PeerOut {
+  static constexpr int kMax = 7;  // SA_MAX_PEERS
+  __nv_bfloat16* ptr[kMax];
+  int n;
+};
+
 // Lazy rescale threshold (log2 units): unnormalised P stays <= 2^8.
 constexpr float kK3RescaleThreshold = 8.0f;
 
@@ -89,7 +97,7 @@ __device__ __forceinline__ uint64_t k3_exp_pair(float y0, float y1, int fr, int 
 
 __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBars& b, uint32_t tS0,
                                                 uint32_t tO0, int quad, int S, __nv_bfloat16* out,
-                                                float* lse, long long* touched, unsigned* status) {
+                                                const K3PeerOut& peers, float* lse, long long* touched, unsigned* status) {
   const int i = quad * 32 + lane_id();  // query row within the tile
   const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
   const uint32_t tS = tS0 + lane_off, tO = tO0 + lane_off;
@@ -381,6 +389,12 @@ __device__ __forceinline__ void k3_softmax_tile(const K3Tile& T, const K3TileBar
 #pragma unroll
       for (int t = 0; t < 4; ++t)
         st_global_v4_hint(d4 + t, make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]), stream_out);
+      // the gather: the same row into every peer's buffer (remote stores over NVLink)
+      for (int p = 0; p < peers.n; ++p) {
+        uint4* r4 = reinterpret_cast<uint4*>(peers.ptr[p] + ((size_t)T.h * S + row) * 128 + ch * 32);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) r4[t] = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+      }
     }
   }
   if (valid && lse) lse[(size_t)T.h * S + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;

@@ -55,6 +55,7 @@ struct ShareParams {
   const int* kv_idx;
   const int* units;  // [n_units][2] items, or null for the natural unit order
   __nv_bfloat16* out;
+  K3PeerOut peers;  // gather fused into the epilogue (sa_sparse_forward_peers)
   float* lse;
   long long* touched;
   unsigned* status;
@@ -115,7 +116,7 @@ struct UnionWalk {
 
 __global__ void __launch_bounds__(kThreads, 1)
     k3_share(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-             const __grid_constant__ CUtensorMap tm_v, const ShareParams P) {
+             const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ ShareParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -298,7 +299,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const K3Tile Tx = x ? T[1] : T[0];  // select, not a dynamically indexed (local-memory) array
     if (Tx.n > 0) {
       const K3TileBars b{&sm->s_full[x], &sm->pv_half[x], &sm->p_part[x], &sm->p_full[x], &sm->o_full[x]};
-      k3_softmax_tile(Tx, b, x ? tS[1] : tS[0], x ? tO[1] : tO[0], warp & 3, P.S, P.out, P.lse, P.touched, P.status);
+      k3_softmax_tile(Tx, b, x ? tS[1] : tS[0], x ? tO[1] : tO[0], warp & 3, P.S, P.out, P.peers, P.lse, P.touched,
+                      P.status);
     } else if ((x ? ib : ia) >= 0 && warp == 4 + 4 * x && lane_id() == 0) {
       report_status(P.status, SA_STATUS_EMPTY_BLOCK, Tx.h, Tx.qb);  // ref executor.py:131-132
     }
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 int launch_sparse_share(const void* q, const void* k, const void* v, int S, int Hq, int Hkv, int group,
                         int q_head0, const int* kv_cnt, const int* kv_idx, const int* units, void* out,
-                        float* lse, long long* touched, cudaStream_t st) {
+                        float* lse, long long* touched, cudaStream_t st, void* const* peer_out, int n_peer) {
   CUtensorMap tq, tk, tv;
   if (!make_tmap_bf16_hsd(&tq, q, Hq, S, 128) || !make_tmap_bf16_hsd(&tk, k, Hkv, S, 128) ||
       !make_tmap_bf16_hsd(&tv, v, Hkv, S, 128))
@@ -330,6 +332,9 @@ int launch_sparse_share(const void* q, const void* k, const void* v, int S, int 
   P.kv_idx = kv_idx;
   P.units = units;
   P.out = static_cast<__nv_bfloat16*>(out);
+  P.peers.n = n_peer;
+  for (int p = 0; p < K3PeerOut::kMax; ++p)
+    P.peers.ptr[p] = p < n_peer ? static_cast<__nv_bfloat16*>(peer_out[p]) : nullptr;
   P.lse = lse;
   P.touched = touched;
   P.status = status_ptr();

@@ -4,20 +4,26 @@ Stages 1-3 are independent per q head (the reference loops heads
 independently, pkg/src/blocksift/pipeline.py:169; the paper partitions heads
 beyond 256K), so a job of Hq heads over N ranks gives rank r
 the contiguous q heads [r*Hq/N, (r+1)*Hq/N) plus the KV heads they read, and
-nothing crosses GPUs on the hot path.  The only collective is the optional
-gather of the per-rank outputs (the 1M-token configuration), done with NCCL
-all-gather over NVLink and overlapped with the next head chunk's compute.
+nothing crosses GPUs on the hot path.  The only exchange is the optional
+gather of the per-rank outputs (the 1M-token configuration).  On GPUs it is
+fused into stage 3: the ranks map each other's gather buffers (CUDA IPC over
+NVLink / NVSwitch, PeerGather) and the K3 epilogue stores every finished
+output row into all of them, so the transfer overlaps the attention tile by
+tile (sa_sparse_forward_peers).  Elsewhere (CPU tensors, the gloo tests) the
+rows are broadcast from their owner after each head chunk.
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
 
+from . import _lib
 from .errors import InputError
 
-__all__ = ["HeadShard", "shard_heads", "sample_attention_sharded"]
+__all__ = ["HeadShard", "shard_heads", "sample_attention_sharded", "PeerGather"]
 
 
 @dataclass(frozen=True)
@@ -52,16 +58,69 @@ def shard_heads(Hq: int, Hkv: int, world: int, rank: int) -> HeadShard:
     return HeadShard(rank, world, q, kv, group)
 
 
+class PeerGather:
+    """Every rank's gather buffer mapped into this process.  Built
+    collectively: each rank exports the CUDA IPC handle (+ byte offset) of its
+    buffer, all ranks exchange them, and the peers' handles are opened once per
+    allocation (cached, since opening an IPC mapping costs milliseconds).
+    addr[r] is the device address of rank r's buffer (this rank's own pointer
+    for r == rank)."""
+
+    _opened: dict = {}  # (peer handle bytes) -> mapped base address
+
+    def __init__(self, full: torch.Tensor, rank: int, world: int, process_group=None):
+        import torch.distributed as dist
+
+        handle = (ctypes.c_char * _lib.SA_IPC_HANDLE_BYTES)()
+        off = ctypes.c_ulonglong(0)
+        with torch.cuda.device(full.device):
+            _lib.call("sa_ipc_export", ctypes.c_void_p(full.data_ptr()), handle, ctypes.byref(off))
+        got = [None] * world
+        dist.all_gather_object(got, (bytes(handle), int(off.value)), group=process_group)
+        self.addr = []
+        for r, (h, o) in enumerate(got):
+            if r == rank:
+                self.addr.append(full.data_ptr())
+                continue
+            base = PeerGather._opened.get(h)
+            if base is None:
+                ptr = ctypes.c_void_p()
+                with torch.cuda.device(full.device):
+                    _lib.call("sa_ipc_open", ctypes.create_string_buffer(h, len(h)), ctypes.byref(ptr))
+                base = PeerGather._opened[h] = int(ptr.value)
+            self.addr.append(base + o)
+        self.rank, self.world = rank, world
+
+    def peers_at(self, byte_offset: int) -> list:
+        """The other ranks' addresses of the same element of their buffers."""
+        return [a + byte_offset for r, a in enumerate(self.addr) if r != self.rank]
+
+    @classmethod
+    def close_all(cls) -> None:
+        for base in cls._opened.values():
+            _lib.call("sa_ipc_close", ctypes.c_void_p(base))
+        cls._opened.clear()
+
+
 def sample_attention_sharded(q_local: torch.Tensor, k_local: torch.Tensor, v_local: torch.Tensor,
                              shard: HeadShard, heads_per_chunk: int = 1, gather: bool = True,
-                             process_group=None, compute_fn=None, out: torch.Tensor | None = None, **kw):
+                             process_group=None, compute_fn=None, out: torch.Tensor | None = None,
+                             transport: str = "auto", **kw):
     """Run this rank's heads in chunks of `heads_per_chunk`.  With gather, the
     job's output [Hq,S,d] is allocated once and this rank computes straight
-    into its own head rows; after each chunk every rank's rows of that chunk
-    are broadcast in place from their owner (one NCCL broadcast per rank, on a
-    side stream for CUDA tensors, so the NVLink transfer overlaps the next
-    chunk's compute).  No temporaries, no copies: a head's rows are a
-    contiguous slice of the final buffer.  Nothing synchronises the host.
+    into its own head rows; every rank's rows reach every other rank's buffer:
+      transport "p2p" (the default for bf16 CUDA tensors): stage 3 stores each
+        finished output row into the peers' buffers too (PeerGather, CUDA IPC
+        over NVLink), so the gather overlaps the attention tile by tile and no
+        collective runs on the data path; the call ends with a stream sync and
+        a barrier, after which every buffer holds every rank's rows (it also
+        starts with one, so no rank writes into a buffer a peer still reads);
+      transport "collective": after each chunk every rank's rows of that chunk
+        are broadcast in place from their owner (one broadcast per rank, on a
+        side stream for CUDA tensors, overlapping the next chunk's compute;
+        nothing synchronises the host).
+    No temporaries, no copies: a head's rows are a contiguous slice of the
+    final buffer.
 
     compute_fn(q, k, v, q_head0=, group=, out=, **kw) defaults to
     sample_attention with check_inputs=False (no host sync per chunk); the CPU
@@ -91,6 +150,17 @@ def sample_attention_sharded(q_local: torch.Tensor, k_local: torch.Tensor, v_loc
         full = None
         mine = out if out is not None else torch.empty_like(q_local)
     on_gpu = q_local.is_cuda
+    if transport == "auto":
+        transport = "p2p" if (on_gpu and q_local.dtype == torch.bfloat16) else "collective"
+    if transport not in ("p2p", "collective"):
+        raise InputError(f"unknown transport {transport!r}")
+    if do_gather and transport == "p2p":
+        if not on_gpu:
+            raise InputError("the p2p gather needs CUDA tensors")
+        if world - 1 > _lib.SA_MAX_PEERS:
+            raise InputError(f"the p2p gather supports up to {_lib.SA_MAX_PEERS + 1} ranks")
+        return _sharded_p2p(q_local, k_local, v_local, shard, heads_per_chunk, full, mine, process_group,
+                            compute_fn, kw)
     comm = torch.cuda.Stream(device=q_local.device) if (do_gather and on_gpu) else None
     main = torch.cuda.current_stream(q_local.device) if on_gpu else None
     works = []
@@ -119,6 +189,26 @@ def sample_attention_sharded(q_local: torch.Tensor, k_local: torch.Tensor, v_loc
     if comm is not None:
         main.wait_stream(comm)
         full.record_stream(comm)
+    return mine, full
+
+
+def _sharded_p2p(q_local, k_local, v_local, shard, heads_per_chunk, full, mine, process_group, compute_fn, kw):
+    import torch.distributed as dist
+
+    H, S, d = q_local.shape
+    dev = q_local.device
+    torch.cuda.current_stream(dev).synchronize()  # no rank writes into a buffer a peer may still be reading
+    peers = PeerGather(full, shard.rank, shard.world, process_group)  # collective: also the entry barrier
+    row_bytes = S * d * full.element_size()
+    for h0 in range(0, H, heads_per_chunk):
+        h1 = min(H, h0 + heads_per_chunk)
+        g0 = shard.q_heads[h0]
+        kv0 = shard.local_kv(g0)
+        kv1 = shard.local_kv(shard.q_heads[h1 - 1]) + 1
+        compute_fn(q_local[h0:h1], k_local[kv0:kv1], v_local[kv0:kv1], q_head0=g0, group=shard.group,
+                   out=mine[h0:h1], peer_out=peers.peers_at((shard.rank * H + h0) * row_bytes), **kw)
+    torch.cuda.current_stream(dev).synchronize()  # this rank's remote stores have landed
+    dist.barrier(group=process_group)              # ... and every peer's
     return mine, full
 
 

@@ -58,7 +58,7 @@ def sample_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, alpha: f
                      sample_ratio: float | None = None, blk: int = 128, sink_blocks: int = 0,
                      local_blocks: int = 1, guard: str = "auto", check_inputs: bool = True,
                      return_lse: bool = False, timings: bool = False, q_head0: int = 0,
-                     group: int | None = None, out: torch.Tensor | None = None):
+                     group: int | None = None, out: torch.Tensor | None = None, peer_out: list | None = None):
     """SampleAttention prefill for q [Hq,S,d], k/v [Hkv,S,d] (bf16 or fp32, CUDA).
 
     alpha: CRA threshold (alpha_c = alpha_s = alpha unless given);
@@ -69,7 +69,8 @@ def sample_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, alpha: f
     check_inputs: scan q/k/v for NaN/Inf (InputError, ref core.py:30-37) and
     read the stage-3 invariant status (ref executor.py:131-132, 150-153); both
     are device flags read with ONE host sync after every stage is enqueued.
-    check_inputs=False leaves the call free of host synchronisation."""
+    check_inputs=False leaves the call free of host synchronisation.
+    peer_out: the output gather fused into stage 3 (parallel.sample_attention_sharded)."""
     batch = HeadBatch.from_tensors(q, k, v, group=group, q_head0=q_head0)
     flag = None
     rescan = None
@@ -91,7 +92,7 @@ def sample_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, alpha: f
     if ev:
         ev[2].record()
     lse = torch.empty((batch.Hq, batch.S), dtype=torch.float32, device=batch.q.device) if return_lse else None
-    o, _ = sparse_attention(batch, mask, out=out, lse=lse, report=False)
+    o, _ = sparse_attention(batch, mask, out=out, lse=lse, report=False, peer_out=peer_out)
     if ev:
         ev[3].record()
     if check_inputs:

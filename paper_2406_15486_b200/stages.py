@@ -20,6 +20,8 @@ exact stage 1 for every pair; "never" skips the guard.
 
 from __future__ import annotations
 
+import ctypes
+
 import contextlib
 from dataclasses import dataclass, field
 
@@ -445,14 +447,18 @@ def _check_buffer(name: str, t: torch.Tensor, shape: tuple, dtype, device) -> No
 
 
 def sparse_attention(heads, mask: BlockMask, out: torch.Tensor | None = None,
-                     lse: torch.Tensor | None = None, report: bool = True, check: bool | None = None):
+                     lse: torch.Tensor | None = None, report: bool = True, check: bool | None = None,
+                     peer_out: list | None = None):
     """Block-sparse causal attention over the mask's active blocks
     (executor.py:104-158).  Returns (out [H, S, d] in the input dtype,
     FlopReport with the kernel's touched-block count and wall_time_sparse,
     the kernel's CUDA-event time) — or (out, None) with report=False, which
     keeps the call free of host synchronisation.  check (default: report)
     reads the device status word and raises the reference's errors for an
-    empty query block / broken mask invariants / empty normaliser."""
+    empty query block / broken mask invariants / empty normaliser.
+    peer_out: device addresses (peer-mapped, parallel.PeerGather) of the same
+    rows in other ranks' gather buffers; the kernel stores every output row
+    there too, tile by tile (sa_sparse_forward_peers, bf16 only)."""
     b = as_batch(heads)
     if check is None:
         check = report
@@ -471,10 +477,14 @@ def sparse_attention(heads, mask: BlockMask, out: torch.Tensor | None = None,
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if report else None
     if ev:
         ev[0].record()
-    dcall(b.q.device, "sa_sparse_forward", b.q.data_ptr(), b.k.data_ptr(), b.v.data_ptr(), b.dtype_code, b.S, b.Hq,
-              b.Hkv, b.d, mask.blk, b.group, b.q_head0, mask.kv_cnt.data_ptr(), mask.kv_idx.data_ptr(),
-              mask.order(b.group, b.q_head0).data_ptr(), out.data_ptr(), None if lse is None else lse.data_ptr(),
-              None if touched is None else touched.data_ptr(), b.stream)
+    args = (b.q.data_ptr(), b.k.data_ptr(), b.v.data_ptr(), b.dtype_code, b.S, b.Hq, b.Hkv, b.d, mask.blk, b.group,
+            b.q_head0, mask.kv_cnt.data_ptr(), mask.kv_idx.data_ptr(), mask.order(b.group, b.q_head0).data_ptr(),
+            out.data_ptr(), None if lse is None else lse.data_ptr(), None if touched is None else touched.data_ptr())
+    if peer_out:
+        arr = (ctypes.c_void_p * len(peer_out))(*[int(p) for p in peer_out])
+        dcall(b.q.device, "sa_sparse_forward_peers", *args, arr, len(peer_out), b.stream)
+    else:
+        dcall(b.q.device, "sa_sparse_forward", *args, b.stream)
     if ev:
         ev[1].record()
     if check:

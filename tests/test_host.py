@@ -1,6 +1,7 @@
 """CPU-side checks: the C-ABI library loads and exports every declared
 symbol, and the host integer logic (config, plan) matches the pinned oracle."""
 
+import ctypes
 import os
 import re
 
@@ -126,6 +127,20 @@ def test_c_abi_rejects_bad_arguments_without_touching_the_gpu():
     rc = lib.sa_sparse_forward(fake, fake, fake, _lib.SA_FP32, 512, 1, 1, 256, 128, 1, 0, fake, fake, None, fake,
                                None, None, None)
     assert rc == _lib.SA_ERR_UNSUPPORTED
+    # stage 3 with the fused gather: peer count, peer pointers and dtype are checked before any launch
+    P = ctypes.c_void_p
+    peers8 = (P * 8)(*([fake] * 8))
+    assert lib.sa_sparse_forward_peers(fake, fake, fake, _lib.SA_BF16, 4096, 2, 1, 128, 128, 2, 0, fake, fake, None,
+                                       fake, None, None, peers8, 8, None) == _lib.SA_ERR_INVALID
+    assert "n_peer" in _err(lib)
+    assert lib.sa_sparse_forward_peers(fake, fake, fake, _lib.SA_BF16, 4096, 2, 1, 128, 128, 2, 0, fake, fake, None,
+                                       fake, None, None, (P * 1)(None), 1, None) == _lib.SA_ERR_INVALID
+    assert "null peer" in _err(lib)
+    assert lib.sa_sparse_forward_peers(fake, fake, fake, _lib.SA_FP32, 4096, 2, 1, 128, 128, 2, 0, fake, fake, None,
+                                       fake, None, None, peers8, 1, None) == _lib.SA_ERR_UNSUPPORTED
+    assert lib.sa_ipc_export(None, None, None) == _lib.SA_ERR_INVALID
+    assert lib.sa_ipc_open(None, None) == _lib.SA_ERR_INVALID
+    assert lib.sa_ipc_close(None) == _lib.SA_ERR_INVALID
     # the Python wrapper turns these codes into the reference's exception types
     with pytest.raises(sa.InputError):
         _lib.call("sa_schedule", None, None, 1, 1, 1, 0, None, None, None)
