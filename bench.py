@@ -337,7 +337,8 @@ def main():
                 masks.append(r_.mask)
                 return o_, r_
 
-            sample_attention_sharded(q, k, v, shard, heads_per_chunk=1, compute_fn=fn, alpha=alpha,
+            # the gather rides on stage 3's stores (p2p), so all of this rank's heads go in one call
+            sample_attention_sharded(q, k, v, shard, heads_per_chunk=len(shard.q_heads), compute_fn=fn, alpha=alpha,
                                      chunk_n=chunk_n, guard=args.guard, out=gather_buf)
             return out, _Res(masks)
         return sa.sample_attention(q, k, v, alpha=alpha, chunk_n=chunk_n, guard=args.guard, timings=timings,

@@ -42,8 +42,15 @@ constexpr uint32_t kBoxBytes = kTileBytes / 2;
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, false);
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 128, true);
 
+// K / V ring depths (K and V tiles are released separately).  A third K or V
+// stage (224 KB of smem) measured the same at C3, C3 dense and C2
+// (profiles/r2/s3/k3_ring_*.txt): the issuer waits ~45 / ~75 cycles per
+// item-block on K / V, the loads are not what holds the MMAs back.
+constexpr int kKSt = 2, kVSt = 2;
+static_assert((2 + kKSt + kVSt) * 32768 + 1024 + 256 <= 232448, "K3 smem over the 227 KB opt-in limit");
+
 struct __align__(8) ShareSmem {
-  uint64_t q_full[2], k_full[2], k_empty[2], v_full[2], v_empty[2];
+  uint64_t q_full[2], k_full[kKSt], k_empty[kKSt], v_full[kVSt], v_empty[kVSt];
   uint64_t s_full[2], p_part[2], p_full[2], o_full[2];  // p_part/p_full = P of keys 0..63 / all keys
   uint64_t pv_half[2];                                    // PV over keys 0..63 of the current block done
   uint32_t tmem_base;
@@ -121,9 +128,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* sQ[2] = {base, base + kTileBytes};
-  unsigned char* const sK0 = base + 2 * kTileBytes;  // K stage s at sK0 + s * kTileBytes
-  unsigned char* const sV0 = base + 4 * kTileBytes;  // V stage s at sV0 + s * kTileBytes
-  ShareSmem* sm = reinterpret_cast<ShareSmem*>(base + 6 * kTileBytes);
+  unsigned char* const sK0 = base + 2 * kTileBytes;           // K stage s at sK0 + s * kTileBytes
+  unsigned char* const sV0 = base + (2 + kKSt) * kTileBytes;  // V stage s at sV0 + s * kTileBytes
+  ShareSmem* sm = reinterpret_cast<ShareSmem*>(base + (2 + kKSt + kVSt) * kTileBytes);
   const int warp = warp_id();
   int ia, ib;
   unit_of(P, blockIdx.x, ia, ib);
@@ -133,12 +140,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
-    for (int x = 0; x < 2; ++x) {
-      mbar_init(&sm->q_full[x], 1);
+    for (int x = 0; x < kKSt; ++x) {
       mbar_init(&sm->k_full[x], 1);
       mbar_init(&sm->k_empty[x], 1);
+    }
+    for (int x = 0; x < kVSt; ++x) {
       mbar_init(&sm->v_full[x], 1);
       mbar_init(&sm->v_empty[x], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&sm->q_full[x], 1);
       mbar_init(&sm->s_full[x], 1);
       mbar_init(&sm->p_part[x], 4);  // one arrive per softmax warp
       mbar_init(&sm->p_full[x], 4);
@@ -172,23 +183,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       int kb;
       bool inA, inB;
       K3Prof pf;
+      int sk = 0, pk = 0, sv = 0, pv = 0;  // ring slot and its wrap count (phase) for K and V
       for (int t = 0; w.next(kb, inA, inB); ++t) {
-        const int s = t & 1;
         const int key0 = kb * 128;
         pf.start();
-        if (t >= 2) k3_wait(&sm->k_empty[s], ((t - 2) >> 1) & 1);
+        if (t >= kKSt) k3_wait(&sm->k_empty[sk], (pk - 1) & 1);
         pf.stop(10);
-        mbar_expect_tx(&sm->k_full[s], kTileBytes);
-        unsigned char* sK = sK0 + s * kTileBytes;
-        tma_load_3d_hint(sK, &tm_k, &sm->k_full[s], 0, key0, kvh, keep);
-        tma_load_3d_hint(sK + kBoxBytes, &tm_k, &sm->k_full[s], 64, key0, kvh, keep);
+        mbar_expect_tx(&sm->k_full[sk], kTileBytes);
+        unsigned char* sK = sK0 + sk * kTileBytes;
+        tma_load_3d_hint(sK, &tm_k, &sm->k_full[sk], 0, key0, kvh, keep);
+        tma_load_3d_hint(sK + kBoxBytes, &tm_k, &sm->k_full[sk], 64, key0, kvh, keep);
         pf.start();
-        if (t >= 2) k3_wait(&sm->v_empty[s], ((t - 2) >> 1) & 1);
+        if (t >= kVSt) k3_wait(&sm->v_empty[sv], (pv - 1) & 1);
         pf.stop(11);
-        mbar_expect_tx(&sm->v_full[s], kTileBytes);
-        unsigned char* sV = sV0 + s * kTileBytes;
-        tma_load_3d_hint(sV, &tm_v, &sm->v_full[s], 0, key0, kvh, keep);
-        tma_load_3d_hint(sV + kBoxBytes, &tm_v, &sm->v_full[s], 64, key0, kvh, keep);
+        mbar_expect_tx(&sm->v_full[sv], kTileBytes);
+        unsigned char* sV = sV0 + sv * kTileBytes;
+        tma_load_3d_hint(sV, &tm_v, &sm->v_full[sv], 0, key0, kvh, keep);
+        tma_load_3d_hint(sV + kBoxBytes, &tm_v, &sm->v_full[sv], 64, key0, kvh, keep);
+        if (++sk == kKSt) sk = 0, ++pk;
+        if (++sv == kVSt) sv = 0, ++pv;
       }
       pf.flush(true);
     }
@@ -213,12 +226,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // O_X += P_X V(step): keys 0..63 once that half of P is in TMEM, 64..127 after
     auto issue_pv = [&](int x, int step) {
       const int j = n_pv[x];
-      const int s = step & 1;
+      const int s = step % kVSt;
       pf.start();
       k3_wait(&sm->p_part[x], j & 1);
       pf.stop(5);
       pf.start();
-      k3_wait(&sm->v_full[s], (step >> 1) & 1);
+      k3_wait(&sm->v_full[s], (step / kVSt) & 1);
       pf.stop(7);
       tc_fence_after();
       if (elect_one()) {
@@ -263,10 +276,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       ++n_s[x];
     };
+    int sk = 0, pk = 0;  // K ring slot of step t and its wrap count
     while (w.next(kb, in[0], in[1])) {
-      const int s = t & 1;
+      const int s = sk;
       pf.start();
-      k3_wait(&sm->k_full[s], (t >> 1) & 1);
+      k3_wait(&sm->k_full[s], pk & 1);
       pf.stop(8);
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
@@ -281,10 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (elect_one()) {
         umma_commit(&sm->k_empty[s]);
-        if (t >= 1) umma_commit(&sm->v_empty[s ^ 1]);  // every PV of step t-1 is issued by now
+        if (t >= 1) umma_commit(&sm->v_empty[(t - 1) % kVSt]);  // every PV of step t-1 is issued by now
       }
       __syncwarp();
       ++t;
+      if (++sk == kKSt) sk = 0, ++pk;
     }
 #pragma unroll
     for (int x = 0; x < 2; ++x)
@@ -338,7 +353,7 @@ int launch_sparse_share(const void* q, const void* k, const void* v, int S, int 
   P.lse = lse;
   P.touched = touched;
   P.status = status_ptr();
-  const size_t smem = 6 * (size_t)kTileBytes + sizeof(ShareSmem) + 1024;
+  const size_t smem = (2 + kKSt + kVSt) * (size_t)kTileBytes + sizeof(ShareSmem) + 1024;
   set_smem_attr(reinterpret_cast<const void*>(&k3_share), (int)smem);
   if (touched) cudaMemsetAsync(touched, 0, sizeof(long long) * Hq, st);
   const int nu = n_units(Hq, P.nb, group, q_head0);
