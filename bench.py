@@ -257,6 +257,8 @@ def main():
     d = 128
     workload = {"workload": describe(desc, S, alpha, chunk_n), "S": S, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d, "alpha": alpha,
                 "chunk_n": chunk_n, "blk": 128, "parallelism": f"heads/{world}" + ("+gather" if gather else ""),
+                **({"gather": "fused into stage 3: each rank's K3 epilogue stores its rows into every peer's "
+                              "output over NVLink (CUDA IPC mapped buffers)"} if gather and world > 1 else {}),
                 "l2": "flushed between steps"}
 
     if args.dry_run:
