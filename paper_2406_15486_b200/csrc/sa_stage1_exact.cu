@@ -472,6 +472,9 @@ int launch_band_ties(const Stage1Geom& g, const int* band, int* flags, const dou
   return check_launch("band refinement: per-row tie certificate");
 }
 
+// loads issued per batch in the fold / row-statistics kernels (4 beat 8 and 16
+// in profiles/r2/s3/foldb_*.txt)
+constexpr int kRowfinBatch = 4;
 // Per sampled row: global max M and normaliser L over the row's key blocks.
 // One warp per row, lanes stride the key blocks; fixed shuffle tree.
 // TPlane = float with log2-domain maxima (tensor-core partials) or double
@@ -489,9 +492,23 @@ __device__ __forceinline__ void rowfin_pair(Stage1Geom g, int hc, const TPlane* 
     for (int kb = lane; kb < w.nkb; kb += 32) mx = fmax(mx, (double)pm[o + kb]);
     for (int s = 16; s > 0; s >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, s));
     double L = 0.0;
-    for (int kb = lane; kb < w.nkb; kb += 32) {
-      const double m = (double)pm[o + kb];
-      if (m != -INFINITY) L += ((double)pa[o + kb] + (double)pb[o + kb]) * (kLog2 ? exp2(m - mx) : exp(m - mx));
+    // the lane's key blocks in batches of 4: loads first, then the sums in order
+    for (int kb0 = lane; kb0 < w.nkb; kb0 += kRowfinBatch * 32) {
+      TPlane m_[kRowfinBatch], ab_[kRowfinBatch][2];
+#pragma unroll
+      for (int u = 0; u < kRowfinBatch; ++u) {
+        const int kb = kb0 + 32 * u;
+        const bool in = kb < w.nkb;
+        m_[u] = in ? pm[o + kb] : (TPlane)-INFINITY;
+        ab_[u][0] = in ? pa[o + kb] : (TPlane)0;
+        ab_[u][1] = in ? pb[o + kb] : (TPlane)0;
+      }
+#pragma unroll
+      for (int u = 0; u < kRowfinBatch; ++u) {
+        const double m = (double)m_[u];
+        if (m != -INFINITY)
+          L += ((double)ab_[u][0] + (double)ab_[u][1]) * (kLog2 ? exp2(m - mx) : exp(m - mx));
+      }
     }
     for (int s = 16; s > 0; s >>= 1) L += __shfl_xor_sync(0xffffffffu, L, s);
     if (lane == 0) {
@@ -519,7 +536,7 @@ __global__ void s1_rowfin(Stage1Geom g, const int* __restrict__ list, const TPla
 // are added in group order, so the result is deterministic.  (A thread per
 // key block looping over all 128 rows left the fold latency-bound: ~140 us
 // at C3 for 50 MB.)
-constexpr int kFoldKb = 32, kFoldGroups = 8;
+constexpr int kFoldKb = 32, kFoldGroups = 8, kFoldBatch = 4;
 
 template <typename TPlane, bool kLog2>
 __device__ __forceinline__ void fold_pair(Stage1Geom g, int hc, const TPlane* __restrict__ pa,
@@ -540,16 +557,30 @@ __device__ __forceinline__ void fold_pair(Stage1Geom g, int hc, const TPlane* __
   double s4[4] = {0.0, 0.0, 0.0, 0.0};
   if (kb < w.nkb) {
     const int r1 = min(nr, (grp + 1) * per);
-    for (int r = grp * per; r < r1; ++r) {
-      const size_t o = ((size_t)hc * g.blk + r) * g.nb + kb;
-      const double m = (double)pm[o];
-      if (m == -INFINITY) continue;
-      const double wgt = (kLog2 ? exp2(m - s_w[r][0]) : exp(m - s_w[r][0])) * s_w[r][1];
-      const double a = (double)pa[o] * wgt, b = (double)pb[o] * wgt;
-      const int slot_a = (w.ss + r) / g.blk - b0 + 1;  // bin r//blk - kb, relative to X-1
-      s4[0] += a + b;
-      s4[1 + slot_a] += a;
-      s4[slot_a] += b;  // bin r//blk - kb - 1
+    // rows in batches of kFoldBatch: the batch's loads are issued before any of
+    // its arithmetic (the fold is load-latency bound), rows still added in order
+    for (int rb = grp * per; rb < r1; rb += kFoldBatch) {
+      TPlane m_[kFoldBatch], a_[kFoldBatch], b_[kFoldBatch];
+#pragma unroll
+      for (int u = 0; u < kFoldBatch; ++u) {
+        const size_t o = ((size_t)hc * g.blk + rb + u) * g.nb + kb;
+        const bool in = rb + u < r1;
+        m_[u] = in ? pm[o] : (TPlane)-INFINITY;
+        a_[u] = in ? pa[o] : (TPlane)0;
+        b_[u] = in ? pb[o] : (TPlane)0;
+      }
+#pragma unroll
+      for (int u = 0; u < kFoldBatch; ++u) {
+        const int r = rb + u;
+        const double m = (double)m_[u];
+        if (m == -INFINITY) continue;
+        const double wgt = (kLog2 ? exp2(m - s_w[r][0]) : exp(m - s_w[r][0])) * s_w[r][1];
+        const double a = (double)a_[u] * wgt, b = (double)b_[u] * wgt;
+        const int slot_a = (w.ss + r) / g.blk - b0 + 1;  // bin r//blk - kb, relative to X-1
+        s4[0] += a + b;
+        s4[1 + slot_a] += a;
+        s4[slot_a] += b;  // bin r//blk - kb - 1
+      }
     }
   }
 #pragma unroll
