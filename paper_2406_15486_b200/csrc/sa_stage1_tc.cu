@@ -197,6 +197,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         uint32_t(&r)[32] = rb[ch & 1];
         tmem_ld_wait_regs(r);
         if (ch < 3) tmem_ld32(taddr + (ch + 1) * 32, rb[(ch + 1) & 1]);
+        if (ch == 3) {  // every S value of this block is in registers: the next QK^T may overwrite S
+          // (released before the last 32 exponentials: stage 1 -3..4 %, profiles/r2/s3/k1er_*.txt)
+          tc_fence_before();
+          mbar_arrive(&sm->s_empty[buf]);
+        }
         if (full) {  // same values (FFMA2 = two fused FMAs) as the masked loop
           const uint64_t negm = f32x2(-m_new, -m_new), sl2x2 = f32x2(sl2, sl2);
 #pragma unroll
@@ -218,8 +223,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       }
       const float a = (ac[0] + ac[1]) + (ac[2] + ac[3]);
       const float b = (bc[0] + bc[1]) + (bc[2] + bc[3]);
-      tc_fence_before();
-      mbar_arrive(&sm->s_empty[buf]);
       if (valid) {
         P.pa[prow + kb] = a;
         P.pb[prow + kb] = b;
