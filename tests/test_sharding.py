@@ -87,3 +87,15 @@ def test_sharded_gather_matches_single_process(Hq, Hkv):
     for h in range(Hq):
         want = O.run_head(q[h], k[h // group], v[h // group], 0.9, 0.9, 2, 32)["out"]
         np.testing.assert_allclose(full[h], want, rtol=0, atol=1e-12)
+
+
+def test_p2p_transport_needs_cuda_tensors():
+    """The fused p2p gather maps CUDA allocations; CPU tensors must ask for the
+    collective transport (the default picks it for them)."""
+    shard = shard_heads(4, 2, 2, 0)
+    q = torch.zeros((2, 64, 8))
+    k = torch.zeros((1, 64, 8))
+    with pytest.raises(InputError):
+        sample_attention_sharded(q, k, k, shard, transport="p2p", compute_fn=lambda *a, **kw: None)
+    with pytest.raises(InputError):
+        sample_attention_sharded(q, k, k, shard, transport="nvshmem", compute_fn=lambda *a, **kw: None)
