@@ -43,7 +43,9 @@ def _as_host(x) -> torch.Tensor:
 def _group_plan(Hq: int, group: int, hpg: int) -> list:
     """Stage-3 head groups [h0, h1) inside KV-group boundaries.  A head's Q
     crosses PCIe in ~0.6x the time its stage 3 takes (128K), so the groups
-    ramp up (2, 2, 3, 5 heads, then `hpg`): each group's copy hides under the
+    ramp up (1, 1, 2, 3, 5 heads, then `hpg`; the first stage-3 launch waits
+    for one head's Q instead of two: e2e -0.2..0.4 ms at C3 against 2, 2, 3, 5,
+    profiles/r2/s3/e2e_ramp_ab2.txt): each group's copy hides under the
     previous group's kernels.  The last groups shrink (3, 2, then 1 head):
     each group's output copy hides under the next group's kernels and the
     copy after the last kernel is short."""
@@ -57,7 +59,7 @@ def _group_plan(Hq: int, group: int, hpg: int) -> list:
                     tail.insert(0, s)
                     rest -= s
         if g == 0:
-            for s in (2, 2, 3, 5):
+            for s in (1, 1, 2, 3, 5):
                 if rest > s:
                     head.append(s)
                     rest -= s
