@@ -13,19 +13,26 @@ import torch  # noqa: E402
 import paper_2406_15486_b200 as sa  # noqa: E402
 from paper_2406_15486_b200 import streaming, synth  # noqa: E402
 
-RAMPS = [tuple(int(x) for x in r.split(',')) for r in sys.argv[1:]] or [(2, 2, 3, 5), (1, 2, 3, 5), (1, 1, 2, 3, 5), (1, 2, 2, 3, 5)]
+# a variant is "head ramp[/tail ramp]", e.g. 1,1,2,3,5/1,2,3 (the tail ramp lists the last groups from the end)
+def _parse(a):
+    h, _, t = a.partition("/")
+    return (tuple(int(x) for x in h.split(",")), tuple(int(x) for x in t.split(",")) if t else (1, 2, 3))
+
+
+RAMPS = [_parse(r) for r in sys.argv[1:]] or [((2, 2, 3, 5), (1, 2, 3)), ((1, 2, 3, 5), (1, 2, 3)),
+                                              ((1, 1, 2, 3, 5), (1, 2, 3)), ((1, 2, 2, 3, 5), (1, 2, 3))]
 REPS = int(os.environ.get('REPS', '7'))
 orig = streaming._group_plan
 
 
-def plan_with(ramp):
+def plan_with(ramp, tail_ramp=(1, 2, 3)):
     def plan(Hq, group, hpg):
         groups, h0 = [], 0
         n_kv = Hq // group
         for g in range(n_kv):
             rest, head, tail = group, [], []
             if g == n_kv - 1:
-                for s in (1, 2, 3):
+                for s in tail_ramp:
                     if rest > s:
                         tail.insert(0, s)
                         rest -= s
@@ -43,14 +50,14 @@ def plan_with(ramp):
     return plan
 
 
-assert plan_with((2, 2, 3, 5))(32, 16, 4) == orig(32, 16, 4)
+assert plan_with((1, 1, 2, 3, 5))(32, 16, 4) == orig(32, 16, 4)
 q, k, v, _ = synth.make_inputs(131072, 32, 2, 128, seed=0, device="cuda")
 hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
 ho = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
 res = {r: [] for r in RAMPS}
 for rep in range(REPS):
     for r in RAMPS:
-        streaming._group_plan = plan_with(r)
+        streaming._group_plan = plan_with(*r)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         sa.sample_attention_host(hq, hk, hv, alpha=0.95, chunk_n=1, out=ho)
