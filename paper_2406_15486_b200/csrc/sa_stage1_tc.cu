@@ -197,8 +197,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         uint32_t(&r)[32] = rb[ch & 1];
         tmem_ld_wait_regs(r);
         if (ch < 3) tmem_ld32(taddr + (ch + 1) * 32, rb[(ch + 1) & 1]);
-        if (ch == 3) {  // every S value of this block is in registers: the next QK^T may overwrite S
-          // (released before the last 32 exponentials: stage 1 -3..4 %, profiles/r2/s3/k1er_*.txt)
+        if (ch == 2) {
+          // chunk 3 is waited for here too, so every S value of this block is in
+          // registers and the next QK^T may overwrite S before the last 64
+          // exponentials (stage 1 -3..5 %, profiles/r2/s3/k1er_*.txt, k1r2_*.txt)
+          tmem_ld_wait_regs(rb[1]);
           tc_fence_before();
           mbar_arrive(&sm->s_empty[buf]);
         }
