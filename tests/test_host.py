@@ -144,3 +144,21 @@ def test_c_abi_rejects_bad_arguments_without_touching_the_gpu():
     # the Python wrapper turns these codes into the reference's exception types
     with pytest.raises(sa.InputError):
         _lib.call("sa_schedule", None, None, 1, 1, 1, 0, None, None, None)
+
+
+@pytest.mark.parametrize("Hq,group,hpg", [(32, 16, 4), (32, 4, 4), (32, 32, 4), (8, 8, 2), (4, 1, 4), (32, 16, 16)])
+def test_host_path_group_plan(Hq, group, hpg):
+    """Stage-3 head groups of the host-buffer path: contiguous, cover every
+    head once, never straddle a KV group, at most max(hpg, 5) heads, and the
+    first group of the job is a single head when the KV group has several."""
+    from paper_2406_15486_b200.streaming import _group_plan
+
+    groups = _group_plan(Hq, group, hpg)
+    assert groups[0][0] == 0 and groups[-1][1] == Hq
+    for (a0, a1), (b0, _) in zip(groups, groups[1:]):
+        assert a1 == b0
+    for h0, h1 in groups:
+        assert 0 < h1 - h0 <= max(hpg, 5)
+        assert h0 // group == (h1 - 1) // group  # one KV group per launch
+    if group > 1:
+        assert groups[0] == (0, 1)
